@@ -1,0 +1,138 @@
+/*
+ * beast_b200.h -- C ABI of the B200-native IMPALA learner-step library
+ * (libbeast_b200.so).  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *  - Every pointer argument is CALLER-OWNED DEVICE memory unless stated
+ *    otherwise; tensors are contiguous and time-major ((T, B, ...), batch on
+ *    axis 1, rollout.py:116-144).  The library allocates nothing.
+ *  - `stream` is a cudaStream_t (void* here); every entry point only enqueues
+ *    work on it (stream-ordered, re-entrant, no host synchronisation).
+ *  - Return value: BP_OK, or a BP_ERR_* code for argument / launch errors
+ *    (bp_last_error() gives a thread-local message).  Data-dependent
+ *    violations that the reference raises as exceptions are reported by
+ *    OR-ing BP_STATUS_* bits into the device word `status` (nullable); the
+ *    Python layer checks it and raises SchemaError / NonFiniteError.
+ *
+ * Each entry point names the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/beastpipe/).
+ */
+#ifndef BEAST_B200_H_
+#define BEAST_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_OK 0
+#define BP_ERR_ARG 1         /* bad shape / config argument  (reference: SchemaError, ValueError) */
+#define BP_ERR_UNSUPPORTED 2 /* shape outside what the kernels handle */
+#define BP_ERR_LAUNCH 3      /* CUDA launch / driver error */
+
+/* device status word bits */
+#define BP_STATUS_ACTION_RANGE 1u   /* action outside [0, A)       -> SchemaError  (vtrace.py:64-65, rollout.py:184-188) */
+#define BP_STATUS_NONFINITE_IN 2u   /* NaN/inf in an input         -> NonFiniteError (vtrace.py:83-91) */
+#define BP_STATUS_NEG_DISCOUNT 4u   /* discount < 0                -> SchemaError  (vtrace.py:109-110) */
+#define BP_STATUS_NONFINITE_LOSS 8u /* non-finite total loss       -> NonFiniteError (vtrace.py:202-205) */
+#define BP_STATUS_NONFINITE_GRAD 16u/* non-finite gradient         -> NonFiniteError (model.py:251-252) */
+
+int bp_abi_version(void);
+const char* bp_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * V-trace
+ * ------------------------------------------------------------------------- */
+
+/* Fused log-softmax x2 + action gather + clipped rho/c + reverse scan + pg
+ * advantages.  Replaces action_log_rhos (vtrace.py:51-69) followed by
+ * vtrace_targets (vtrace.py:94-128); upstream TorchBeast vtrace.from_logits.
+ *   behavior_logits, target_logits: (T, B, A) f32;  actions: (T, B) int64
+ *   discounts, rewards, values: (T, B) f32;  bootstrap_value: (B) f32
+ *   clip_rho   : rho_bar (delta clip).           INFINITY = no clip (upstream None)
+ *   clip_pg_rho: clip for pg advantages.         beastpipe uses clip_rho here
+ *   clip_c     : c_bar (trace cut). upstream fixes 1.0
+ * Outputs (T, B) f32: vs, pg_advantages, log_rhos, behavior_logp, target_logp
+ * (the last three nullable).  A <= 48, T*min(B,16) <= 6144. */
+int bp_vtrace_from_logits_f32(const float* behavior_logits, const float* target_logits,
+                              const int64_t* actions, const float* discounts,
+                              const float* rewards, const float* values,
+                              const float* bootstrap_value, int T, int B, int A,
+                              float clip_rho, float clip_pg_rho, float clip_c, float* vs,
+                              float* pg_advantages, float* log_rhos, float* behavior_logp,
+                              float* target_logp, unsigned* status, void* stream);
+
+/* V-trace from given log importance weights.  Replaces vtrace_targets
+ * (vtrace.py:94-128); upstream vtrace.from_importance_weights.
+ * clipped_rhos (nullable) receives min(clip_rho, exp(log_rho)) (VtraceResult.clipped_rhos). */
+int bp_vtrace_from_importance_weights_f32(const float* log_rhos, const float* discounts,
+                                          const float* rewards, const float* values,
+                                          const float* bootstrap_value, int T, int B,
+                                          float clip_rho, float clip_pg_rho, float clip_c,
+                                          float* vs, float* pg_advantages,
+                                          float* clipped_rhos, unsigned* status, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused learner loss: V-trace + policy-gradient / baseline / entropy losses
+ * and their exact gradients in one kernel.  Replaces compute_losses
+ * (vtrace.py:224-255) = action_log_rhos + vtrace_targets + losses_from_targets
+ * (vtrace.py:169-221); upstream learn()'s from_logits + compute_*_loss + autograd.
+ *
+ *   learner_logits  : (T, B, A) f32  rows 0..T-1 of the network output
+ *   learner_baseline: (T+1, B) f32   values = rows 0..T-1, bootstrap = row T
+ *   behavior_logits : (T, B, A) f32  already row-aligned by the caller
+ *                     (beastpipe: policy_logits[:-1]; TorchBeast: [1:])
+ *   actions         : (T, B) int64   aligned like behavior_logits
+ *   rewards         : (T, B) f32     reward[1:]
+ *   done            : (T, B) uint8   done[1:] (bool storage); discount is
+ *                     (float)discount * !done exactly (vtrace.py:246)
+ *   reward_clip     : 1 = clamp rewards to [-1, 1] (upstream abs_one)
+ * Outputs
+ *   d_logits  : (T, B, A) f32   d total / d learner_logits
+ *   d_baseline: (T+1, B) f32    d total / d learner_baseline, row T = 0
+ *   vs, pg_advantages: (T, B) f32, nullable
+ *   losses    : 4 doubles on device: pg, baseline(0.5*sum sq), entropy(-sum H), total
+ *   workspace : bp_learner_loss_workspace_bytes(T, B, A) bytes, zeroed ONCE by
+ *               the caller before first use (the kernel leaves it zeroed). */
+size_t bp_learner_loss_workspace_bytes(int T, int B, int A);
+int bp_learner_loss_f32(const float* learner_logits, const float* learner_baseline,
+                        const float* behavior_logits, const int64_t* actions,
+                        const float* rewards, const uint8_t* done, int T, int B, int A,
+                        float discount, float clip_rho, float clip_pg_rho, float clip_c,
+                        float pg_cost, float baseline_cost, float entropy_cost, int reward_clip,
+                        float* d_logits, float* d_baseline, float* vs, float* pg_advantages,
+                        double* losses, void* workspace, unsigned* status, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Optimiser: global-norm clip + RMSProp (eps outside the root, no momentum)
+ * ------------------------------------------------------------------------- */
+
+/* Sum of squares of n f32 gradients into *sumsq (device double), deterministic.
+ * Replaces the norm in clip_global_norm (model.py:224-228). workspace:
+ * bp_sumsq_workspace_bytes(n), zeroed once. */
+size_t bp_sumsq_workspace_bytes(int64_t n);
+int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* workspace, void* stream);
+
+/* In-place clip + RMSProp over flat buffers of n elements.  Replaces
+ * SharedModel.apply_gradients (pipeline.py:247-251) = clip_global_norm
+ * (model.py:224-233) + rmsprop_step (model.py:236-268).
+ *   clip_mode 0: beastpipe -- scale = max_norm/norm only if max_norm > 0 and norm > max_norm
+ *   clip_mode 1: torch clip_grad_norm_ -- scale = min(1, max_norm/(norm + 1e-6))
+ *   clip_mode 2: no clipping
+ * The norm is read from *sumsq on the device (no host sync); a non-finite
+ * norm rejects the whole step (params untouched, BP_STATUS_NONFINITE_GRAD).
+ * square_avg and params are updated in place; grads are overwritten with the
+ * clipped gradients when write_clipped_grads != 0 (torch semantics).
+ * norm_out (nullable, device f32) receives the pre-clip norm.  lr is read
+ * from *lr_dev when non-null (device-side LR schedule), else `lr`. */
+int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t n,
+                        const double* sumsq, float max_norm, int clip_mode, float lr,
+                        const float* lr_dev, float alpha, float eps, int write_clipped_grads,
+                        float* norm_out, unsigned* status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BEAST_B200_H_ */

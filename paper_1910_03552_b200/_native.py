@@ -1,0 +1,85 @@
+"""ctypes binding of libbeast_b200.so (the C ABI in include/beast_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every op raises.  Build with `python -m paper_1910_03552_b200.build`
+(or `__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .errors import NativeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbeast_b200.so")
+
+_lib = None
+
+P = C.c_void_p
+I = C.c_int
+I64 = C.c_int64
+F = C.c_float
+SZ = C.c_size_t
+
+# name -> (restype, argtypes); every symbol include/beast_b200.h declares
+SIGNATURES: dict[str, tuple] = {
+    "bp_abi_version": (I, []),
+    "bp_last_error": (C.c_char_p, []),
+    "bp_vtrace_from_logits_f32": (I, [P, P, P, P, P, P, P, I, I, I, F, F, F, P, P, P, P, P, P, P]),
+    "bp_vtrace_from_importance_weights_f32": (I, [P, P, P, P, P, I, I, F, F, F, P, P, P, P, P]),
+    "bp_learner_loss_workspace_bytes": (SZ, [I, I, I]),
+    "bp_learner_loss_f32": (I, [P, P, P, P, P, P, I, I, I, F, F, F, F, F, F, F, I,
+                                P, P, P, P, P, P, P, P]),
+    "bp_sumsq_workspace_bytes": (SZ, [I64]),
+    "bp_sumsq_f32": (I, [P, I64, P, P, P]),
+    "bp_rmsprop_clip_f32": (I, [P, P, P, I64, P, F, I, F, P, F, F, I, P, P, P]),
+}
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the library. Raises NativeError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeError(
+            f"{path} not built; run `python -m paper_1910_03552_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def lib():
+    return _lib if _lib is not None else load()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().bp_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (code {rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None passes NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def require_cuda(*tensors) -> None:
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the B200 kernels have no CPU fallback")
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise NativeError("expected CUDA tensors")

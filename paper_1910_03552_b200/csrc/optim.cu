@@ -1,0 +1,168 @@
+// Global-norm clip + RMSProp, replacing SharedModel.apply_gradients
+// (pipeline.py:247-251) = clip_global_norm (model.py:224-233) + rmsprop_step
+// (model.py:236-268).  Two HBM-bound passes over flat fp32 buffers:
+//   1. bp_sumsq_f32        : sum g^2 -> device double (deterministic two-level reduce)
+//   2. bp_rmsprop_clip_f32 : reads the norm on device (no host sync), clips and
+//                            updates p / square_avg in place (float4 vectorised).
+#include "common.cuh"
+
+namespace bp {
+
+constexpr int kOptThreads = 256;
+constexpr int kSumsqBlocks = 2 * 148;
+
+__global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
+                                                            double* __restrict__ out,
+                                                            double* __restrict__ partials,
+                                                            unsigned* __restrict__ counter) {
+  const int64_t tid = (int64_t)blockIdx.x * kOptThreads + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kOptThreads;
+  float acc = 0.f;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  if (vec) {
+    const int64_t n4 = n >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = tid; i < n4; i += stride) {
+      const float4 v = __ldcs(x4 + i);
+      acc = fmaf(v.x, v.x, acc);
+      acc = fmaf(v.y, v.y, acc);
+      acc = fmaf(v.z, v.z, acc);
+      acc = fmaf(v.w, v.w, acc);
+    }
+    for (int64_t i = (n4 << 2) + tid; i < n; i += stride) acc = fmaf(x[i], x[i], acc);
+  } else {
+    for (int64_t i = tid; i < n; i += stride) acc = fmaf(x[i], x[i], acc);
+  }
+  double d = warp_sum((double)acc);
+  __shared__ double red[kOptThreads / 32];
+  __shared__ bool is_last;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int k = 0; k < kOptThreads / 32; ++k) s += red[k];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0;
+    for (int k = 0; k < (int)gridDim.x; ++k) s += ((volatile double*)partials)[k];
+    *out = s;
+    *counter = 0u;
+  }
+}
+
+struct ClipScale {
+  float scale;
+  bool ok;
+};
+
+BP_DEVICE ClipScale clip_scale(const double* sumsq, float max_norm, int mode) {
+  const double ss = *sumsq;
+  ClipScale c{1.f, isfinite(ss) != 0};
+  const double norm = sqrt(ss);
+  if (mode == 0) {  // beastpipe model.py:229-232
+    if (max_norm > 0.f && norm > (double)max_norm) c.scale = (float)((double)max_norm / norm);
+  } else if (mode == 1) {  // torch clip_grad_norm_
+    const double coef = (double)max_norm / (norm + 1e-6);
+    c.scale = (float)(coef < 1.0 ? coef : 1.0);
+  }
+  return c;
+}
+
+BP_DEVICE float rms_one(float& p, float g, float& s, float lr, float alpha, float eps) {
+  s = alpha * s + (1.f - alpha) * g * g;
+  const float denom = sqrtf(s) + eps;
+  const float step = denom != 0.f ? g / denom : 0.f;  // model.py:261-262
+  p = p - lr * step;
+  return g;
+}
+
+__global__ void __launch_bounds__(kOptThreads)
+    rmsprop_kernel(float* __restrict__ p, float* __restrict__ g, float* __restrict__ s, int64_t n,
+                   const double* __restrict__ sumsq, float max_norm, int mode, float lr_host,
+                   const float* __restrict__ lr_dev, float alpha, float eps, int write_grads,
+                   float* __restrict__ norm_out, unsigned* status) {
+  const ClipScale cs = clip_scale(sumsq, max_norm, mode);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (norm_out) *norm_out = (float)sqrt(*sumsq);
+    if (!cs.ok) set_status(status, BP_STATUS_NONFINITE_GRAD);
+  }
+  if (!cs.ok) return;  // reject the step, params untouched (model.py:251-252)
+  const float lr = lr_dev ? *lr_dev : lr_host;
+  const float sc = cs.scale;
+  const int64_t tid = (int64_t)blockIdx.x * kOptThreads + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kOptThreads;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(s)) & 15u) == 0;
+  int64_t start = 0;
+  if (vec) {
+    const int64_t n4 = n >> 2;
+    float4* p4 = reinterpret_cast<float4*>(p);
+    float4* g4 = reinterpret_cast<float4*>(g);
+    float4* s4 = reinterpret_cast<float4*>(s);
+    for (int64_t i = tid; i < n4; i += stride) {
+      float4 pv = p4[i], sv = s4[i];
+      float4 gv = __ldcs(g4 + i);
+      gv.x *= sc; gv.y *= sc; gv.z *= sc; gv.w *= sc;
+      rms_one(pv.x, gv.x, sv.x, lr, alpha, eps);
+      rms_one(pv.y, gv.y, sv.y, lr, alpha, eps);
+      rms_one(pv.z, gv.z, sv.z, lr, alpha, eps);
+      rms_one(pv.w, gv.w, sv.w, lr, alpha, eps);
+      p4[i] = pv;
+      s4[i] = sv;
+      if (write_grads) g4[i] = gv;
+    }
+    start = n4 << 2;
+  }
+  for (int64_t i = start + tid; i < n; i += stride) {
+    float pv = p[i], sv = s[i];
+    const float gv = g[i] * sc;
+    rms_one(pv, gv, sv, lr, alpha, eps);
+    p[i] = pv;
+    s[i] = sv;
+    if (write_grads) g[i] = gv;
+  }
+}
+
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" size_t bp_sumsq_workspace_bytes(int64_t n) {
+  (void)n;
+  return 256 + kSumsqBlocks * sizeof(double);
+}
+
+extern "C" int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* workspace, void* stream) {
+  if (n < 0 || !sumsq || !workspace) {
+    set_error("sumsq: bad args");
+    return BP_ERR_ARG;
+  }
+  unsigned* counter = reinterpret_cast<unsigned*>(workspace);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + 256);
+  int64_t want = (n / 4 + kOptThreads - 1) / kOptThreads;
+  int grid = (int)(want < 1 ? 1 : (want > kSumsqBlocks ? kSumsqBlocks : want));
+  sumsq_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(x, n, sumsq, partials, counter);
+  return check_launch("sumsq_kernel");
+}
+
+extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t n,
+                                   const double* sumsq, float max_norm, int clip_mode, float lr,
+                                   const float* lr_dev, float alpha, float eps,
+                                   int write_clipped_grads, float* norm_out, unsigned* status,
+                                   void* stream) {
+  if (n < 0 || !params || !grads || !square_avg || !sumsq || clip_mode < 0 || clip_mode > 2) {
+    set_error("rmsprop_clip: bad args");
+    return BP_ERR_ARG;
+  }
+  int64_t want = (n / 4 + kOptThreads - 1) / kOptThreads;
+  int grid = (int)(want < 1 ? 1 : (want > 4 * 148 ? 4 * 148 : want));
+  rmsprop_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(
+      params, grads, square_avg, n, sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps,
+      write_clipped_grads, norm_out, status);
+  return check_launch("rmsprop_kernel");
+}

@@ -1,0 +1,613 @@
+// Fused V-trace kernels for sm_100a.
+//
+// One kernel family, three modes:
+//   MODE_LOGITS : vtrace.from_logits            (action_log_rhos + vtrace_targets,
+//                                                 beastpipe vtrace.py:51-128)
+//   MODE_IW     : vtrace.from_importance_weights (vtrace_targets, vtrace.py:94-128)
+//   MODE_LOSS   : fused learner loss              (compute_losses, vtrace.py:224-255:
+//                                                 V-trace + losses_from_targets :169-221)
+//
+// Layout: all tensors time-major (T, B[, A]).  A CTA owns a tile of BT batch
+// columns for ALL T rows (columns are independent; the scan runs along T).
+//
+//   phase 1  row-parallel, streamed over T in chunks of TC = 128/BT time rows:
+//            cp.async (LDGSTS) 3-stage ring brings the (TC, BT*A) logits spans
+//            (contiguous per time row) into shared memory; one thread per
+//            (t, b) row computes both log-softmaxes, gathers the action, and
+//            parks log_rho / discount / reward / value in smem scan arrays.
+//   phase 2  parallel delta / c precompute, then the serial reverse scan
+//            acc = delta_t + gamma_t c_t acc (BT threads, FMA chain only),
+//            then parallel vs / pg_advantage outputs.
+//   phase 3  (MODE_LOSS) loss partial sums -> deterministic last-block reduce;
+//            second streamed pass over the learner logits (L2-resident) writes
+//            d_logits through smem with coalesced vector stores.
+#include <cstdio>
+#include <cstdarg>
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bp {
+
+enum { MODE_LOGITS = 0, MODE_IW = 1, MODE_LOSS = 2 };
+
+constexpr int kThreads = 128;  // == rows per chunk
+constexpr int kStages = 3;
+constexpr int kMaxA = 48;
+constexpr int kMaxTB = 2048;  // T * BT bound for the smem scan arrays
+
+struct VtArgs {
+  const float* beh;      // (T,B,A)
+  const float* tgt;      // (T,B,A) target / learner logits
+  const int64_t* act;    // (T,B)
+  const float* disc;     // (T,B)           MODE_LOGITS / MODE_IW
+  const uint8_t* done;   // (T,B) done[1:]  MODE_LOSS
+  const float* rew;      // (T,B)
+  const float* val;      // (T,B) values, or (T+1,B) baseline in MODE_LOSS
+  const float* boot;     // (B)             (MODE_LOSS: val + T*B)
+  const float* lr_in;    // (T,B)           MODE_IW
+  int T, B, A;
+  float clip_rho, clip_pg_rho, clip_c;
+  float discount, pg_cost, baseline_cost, entropy_cost;
+  int reward_clip;
+  float* vs;
+  float* pg;
+  float* log_rhos;
+  float* beh_logp;
+  float* tgt_logp;
+  float* clipped_rhos;
+  float* d_logits;
+  float* d_baseline;
+  double* losses;
+  double* partials;  // gridDim.x * 3
+  unsigned* counter;
+  unsigned* status;
+};
+
+__host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
+
+struct SmemPlan {
+  int TC, RS;            // time rows per chunk, smem row stride (floats)
+  size_t stage_floats;   // per stage, both tensors
+  size_t scan_off;       // float offset of the scan arrays
+  int n_scan;            // number of T*BT arrays
+  size_t bytes;
+};
+
+__host__ __device__ inline SmemPlan make_plan(int mode, int BT, int T, int A) {
+  SmemPlan p;
+  p.TC = kThreads / BT;
+  p.RS = round_up4(BT * A);
+  const int ntens = (mode == MODE_IW) ? 0 : 2;
+  p.stage_floats = (size_t)ntens * p.TC * p.RS;
+  p.scan_off = p.stage_floats * kStages;
+  p.n_scan = (mode == MODE_LOSS) ? 10 : 6;
+  p.bytes = (p.scan_off + (size_t)p.n_scan * T * BT + BT) * sizeof(float);
+  return p;
+}
+
+// issue the cp.async copies of logits chunk c (time rows t0..t0+nt) into a stage
+template <int BT, bool VEC>
+BP_DEVICE void issue_chunk(float* stage, const float* src, int RS, int t0, int nt, int b0,
+                           int bw, int B, int A) {
+  const int span = bw * A;  // floats per time row (contiguous in global)
+  if constexpr (VEC) {
+    const int pieces = span >> 2;
+    const int total = nt * pieces;
+    for (int i = threadIdx.x; i < total; i += kThreads) {
+      const int tr = i / pieces;
+      const int p = i - tr * pieces;
+      cp_async16(stage + tr * RS + 4 * p, src + ((size_t)(t0 + tr) * B + b0) * A + 4 * p);
+    }
+  } else {
+    const int total = nt * span;
+    for (int i = threadIdx.x; i < total; i += kThreads) {
+      const int tr = i / span;
+      const int p = i - tr * span;
+      cp_async4(stage + tr * RS + p, src + ((size_t)(t0 + tr) * B + b0) * A + p);
+    }
+  }
+}
+
+struct RowSoftmax {
+  float lse;     // log sum exp (max-shifted form: m + log s)
+  float xa;      // logit of the action
+  float ent;     // entropy (only when requested)
+  bool finite;
+};
+
+template <bool ENT>
+BP_DEVICE RowSoftmax row_softmax(const float* x, int A, int a) {
+  float m = -INFINITY, sx = 0.f;
+  for (int j = 0; j < A; ++j) {
+    const float v = x[j];
+    m = fmaxf(m, v);
+    sx += v;
+  }
+  float s = 0.f, sxe = 0.f;
+  for (int j = 0; j < A; ++j) {
+    const float z = x[j] - m;
+    const float e = fast_exp(z);
+    s += e;
+    if constexpr (ENT) sxe += e * z;
+  }
+  RowSoftmax r;
+  const float ls = fast_log(s);
+  r.lse = m + ls;
+  r.xa = x[a];
+  r.ent = ENT ? (ls - sxe / s) : 0.f;
+  r.finite = isfinite(sx) && isfinite(r.lse) && (!ENT || isfinite(r.ent));
+  return r;
+}
+
+template <int BT, bool VEC, int MODE>
+__global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
+  extern __shared__ __align__(16) float smem[];
+  const int T = g.T, B = g.B, A = g.A;
+  const int b0 = blockIdx.x * BT;
+  const int bw = min(BT, B - b0);
+  const SmemPlan plan = make_plan(MODE, BT, T, A);
+  const int TC = plan.TC, RS = plan.RS;
+  const int TB = T * BT;
+  float* scan = smem + plan.scan_off;
+  float* s_lr = scan;            // log_rho -> pg rho clip
+  float* s_disc = scan + TB;
+  float* s_rew = scan + 2 * TB;
+  float* s_val = scan + 3 * TB;
+  float* s_delta = scan + 4 * TB;  // delta -> vs - V
+  float* s_dc = scan + 5 * TB;     // gamma*c -> pg advantage
+  float* s_lse = scan + 6 * TB;    // MODE_LOSS: learner log Z
+  float* s_ent = scan + 7 * TB;    //            entropy
+  float* s_tlp = scan + 8 * TB;    //            learner log pi(a)
+  int* s_act = reinterpret_cast<int*>(scan + 9 * TB);
+  float* s_boot = scan + plan.n_scan * TB;
+
+  const int tid = threadIdx.x;
+  const int tl = tid / BT;  // time row within chunk
+  const int bl = tid % BT;  // column within tile
+  unsigned bad = 0;
+
+  if (tid < BT && tid < bw) {
+    const float bv = g.boot[b0 + tid];
+    s_boot[tid] = bv;
+    if (!isfinite(bv)) bad |= BP_STATUS_NONFINITE_IN;
+  }
+
+  // ----------------------------------------------------------------- phase 1
+  const int nchunks = (T + TC - 1) / TC;
+  if constexpr (MODE != MODE_IW) {
+    const float* tens[2] = {g.beh, g.tgt};
+    auto issue = [&](int c) {
+      if (c < nchunks) {
+        float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+        const int t0 = c * TC, nt = min(TC, T - t0);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          issue_chunk<BT, VEC>(st + k * TC * RS, tens[k], RS, t0, nt, b0, bw, B, A);
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+    for (int c = 0; c < nchunks; ++c) {
+      issue(c + kStages - 1);
+      const int t = c * TC + tl;
+      const bool live = (t < T) && (bl < bw);
+      // small per-row inputs: plain loads issued before the wait
+      int64_t a64 = 0;
+      float rv = 0.f, vv = 0.f, dv = 0.f;
+      uint8_t dn = 0;
+      const size_t idx = (size_t)t * B + b0 + bl;
+      if (live) {
+        a64 = g.act[idx];
+        rv = g.rew[idx];
+        vv = g.val[idx];
+        if constexpr (MODE == MODE_LOSS) dn = g.done[idx];
+        else dv = g.disc[idx];
+      }
+      cp_async_wait<kStages - 1>();
+      __syncthreads();
+      if (live) {
+        const float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+        int a = (int)a64;
+        if (a64 < 0 || a64 >= A) {
+          bad |= BP_STATUS_ACTION_RANGE;
+          a = 0;
+        }
+        const RowSoftmax rb = row_softmax<false>(st + tl * RS + bl * A, A, a);
+        const RowSoftmax rt = row_softmax<MODE == MODE_LOSS>(st + TC * RS + tl * RS + bl * A, A, a);
+        const float blp = rb.xa - rb.lse;
+        const float tlp = rt.xa - rt.lse;
+        const float lr = tlp - blp;
+        if constexpr (MODE == MODE_LOSS) {
+          dv = dn ? 0.f : g.discount;  // (float)gamma * ~done, exact
+          if (g.reward_clip) rv = fminf(fmaxf(rv, -1.f), 1.f);
+        } else {
+          if (dv < 0.f) bad |= BP_STATUS_NEG_DISCOUNT;
+        }
+        if (!(rb.finite && rt.finite && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(dv)))
+          bad |= BP_STATUS_NONFINITE_IN;
+        const int si = tl * BT + bl + c * TC * BT;  // == t*BT + bl
+        s_lr[si] = lr;
+        s_disc[si] = dv;
+        s_rew[si] = rv;
+        s_val[si] = vv;
+        if constexpr (MODE == MODE_LOSS) {
+          s_lse[si] = rt.lse;
+          s_ent[si] = rt.ent;
+          s_tlp[si] = tlp;
+          s_act[si] = a;
+        } else {
+          if (g.log_rhos) g.log_rhos[idx] = lr;
+          if (g.beh_logp) g.beh_logp[idx] = blp;
+          if (g.tgt_logp) g.tgt_logp[idx] = tlp;
+        }
+      }
+      __syncthreads();  // stage (c % kStages) may be refilled next iteration
+    }
+  } else {
+    // MODE_IW: only (T,B) inputs -- straight coalesced loads into smem
+    for (int i = tid; i < TB; i += kThreads) {
+      const int t = i / BT, b = i % BT;
+      if (b < bw) {
+        const size_t idx = (size_t)t * B + b0 + b;
+        const float lr = g.lr_in[idx], dv = g.disc[idx], rv = g.rew[idx], vv = g.val[idx];
+        if (dv < 0.f) bad |= BP_STATUS_NEG_DISCOUNT;
+        if (!(isfinite(lr) && isfinite(dv) && isfinite(rv) && isfinite(vv)))
+          bad |= BP_STATUS_NONFINITE_IN;
+        s_lr[i] = lr;
+        s_disc[i] = dv;
+        s_rew[i] = rv;
+        s_val[i] = vv;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ----------------------------------------------------------------- phase 2
+  // 2a: delta_t = min(rho_bar, rho)(r + gamma V_{t+1} - V), gamma*c  (vtrace.py:113-117)
+  for (int i = tid; i < TB; i += kThreads) {
+    const int t = i / BT, b = i % BT;
+    if (b < bw) {
+      const float rho = fast_exp(s_lr[i]);
+      const float cr = fminf(g.clip_rho, rho);
+      const float cc = fminf(g.clip_c, rho);
+      const float vnext = (t + 1 < T) ? s_val[i + BT] : s_boot[b];
+      const float dsc = s_disc[i];
+      s_delta[i] = cr * (s_rew[i] + dsc * vnext - s_val[i]);
+      s_dc[i] = dsc * cc;
+      s_lr[i] = fminf(g.clip_pg_rho, rho);
+      if constexpr (MODE == MODE_IW) {
+        if (g.clipped_rhos) g.clipped_rhos[(size_t)t * B + b0 + b] = cr;
+      }
+    }
+  }
+  __syncthreads();
+  // 2b: serial reverse scan, one thread per column (vtrace.py:119-123)
+  if (tid < bw) {
+    float acc = 0.f;
+    int i = (T - 1) * BT + tid;
+#pragma unroll 4
+    for (int t = T - 1; t >= 0; --t, i -= BT) {
+      acc = fmaf(s_dc[i], acc, s_delta[i]);
+      s_delta[i] = acc;
+    }
+  }
+  __syncthreads();
+  // 2c: vs = acc + V; pg = clip_pg(rho)(r + gamma vs_{t+1} - V) (vtrace.py:124-127)
+  double pg_sum = 0.0, base_sum = 0.0, ent_sum = 0.0;
+  for (int i = tid; i < TB; i += kThreads) {
+    const int t = i / BT, b = i % BT;
+    if (b < bw) {
+      const float v = s_val[i];
+      const float vsv = s_delta[i] + v;
+      const float vs_next = (t + 1 < T) ? (s_delta[i + BT] + s_val[i + BT]) : s_boot[b];
+      const float pgv = s_lr[i] * (s_rew[i] + s_disc[i] * vs_next - v);
+      const size_t idx = (size_t)t * B + b0 + b;
+      if (g.vs) g.vs[idx] = vsv;
+      if (g.pg) g.pg[idx] = pgv;
+      if constexpr (MODE == MODE_LOSS) {
+        s_dc[i] = pgv;  // keep for d_logits
+        const float dvs = vsv - v;
+        pg_sum -= (double)pgv * (double)s_tlp[i];
+        base_sum += 0.5 * (double)dvs * (double)dvs;
+        ent_sum -= (double)s_ent[i];
+        g.d_baseline[idx] = g.baseline_cost * (v - vsv);
+      }
+    }
+  }
+  if constexpr (MODE == MODE_LOSS) {
+    if (tid < bw) g.d_baseline[(size_t)T * B + b0 + tid] = 0.f;  // bootstrap row: stop-grad
+  }
+
+  if constexpr (MODE == MODE_LOSS) {
+    // ------------------------------------------------------- phase 3a: loss sums
+    __shared__ double red[3][kThreads / 32];
+    pg_sum = warp_sum(pg_sum);
+    base_sum = warp_sum(base_sum);
+    ent_sum = warp_sum(ent_sum);
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) {
+      red[0][w] = pg_sum;
+      red[1][w] = base_sum;
+      red[2][w] = ent_sum;
+    }
+    __syncthreads();  // also orders s_dc (pg advantages) for phase 3b
+    __shared__ bool is_last;
+    if (tid == 0) {
+      double a0 = 0, a1 = 0, a2 = 0;
+      for (int k = 0; k < kThreads / 32; ++k) {
+        a0 += red[0][k];
+        a1 += red[1][k];
+        a2 += red[2][k];
+      }
+      g.partials[3 * blockIdx.x + 0] = a0;
+      g.partials[3 * blockIdx.x + 1] = a1;
+      g.partials[3 * blockIdx.x + 2] = a2;
+      __threadfence();
+      const unsigned prev = atomicAdd(g.counter, 1u);
+      is_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last && tid == 0) {
+      __threadfence();
+      double a0 = 0, a1 = 0, a2 = 0;
+      for (int k = 0; k < (int)gridDim.x; ++k) {  // fixed order: deterministic
+        a0 += ((volatile double*)g.partials)[3 * k + 0];
+        a1 += ((volatile double*)g.partials)[3 * k + 1];
+        a2 += ((volatile double*)g.partials)[3 * k + 2];
+      }
+      const double total = (double)g.pg_cost * a0 + (double)g.baseline_cost * a1 +
+                           (double)g.entropy_cost * a2;
+      g.losses[0] = a0;
+      g.losses[1] = a1;
+      g.losses[2] = a2;
+      g.losses[3] = total;
+      if (!isfinite(total)) bad |= BP_STATUS_NONFINITE_LOSS;
+      *g.counter = 0u;  // leave the workspace zeroed (graph-replay safe)
+    }
+
+    // ------------------------------------------------------- phase 3b: d_logits
+    // d = pg_cost*adv*(pi - onehot) + ent_cost*pi*(log pi + H)   (vtrace.py:207-210)
+    auto issue = [&](int c) {
+      if (c < nchunks) {
+        float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+        const int t0 = c * TC, nt = min(TC, T - t0);
+        issue_chunk<BT, VEC>(st, g.tgt, RS, t0, nt, b0, bw, B, A);
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+    for (int c = 0; c < nchunks; ++c) {
+      issue(c + kStages - 1);
+      cp_async_wait<kStages - 1>();
+      __syncthreads();
+      float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+      const int t0 = c * TC, nt = min(TC, T - t0);
+      const int t = t0 + tl;
+      if (t < T && bl < bw) {
+        const int si = t * BT + bl;
+        const float lse = s_lse[si], H = s_ent[si], adv = s_dc[si];
+        const int a = s_act[si];
+        float* x = st + tl * RS + bl * A;
+        const float pa = g.pg_cost * adv, ec = g.entropy_cost;
+        for (int j = 0; j < A; ++j) {
+          const float lp = x[j] - lse;
+          const float p = fast_exp(lp);
+          x[j] = pa * (p - (j == a ? 1.f : 0.f)) + ec * p * (lp + H);
+        }
+      }
+      __syncthreads();
+      // coalesced copy-out of the chunk
+      const int span = bw * A;
+      if constexpr (VEC) {
+        const int pieces = span >> 2, total = nt * pieces;
+        for (int i = tid; i < total; i += kThreads) {
+          const int tr = i / pieces, p = i - tr * pieces;
+          const float4 v = *reinterpret_cast<const float4*>(st + tr * RS + 4 * p);
+          st_cs4(reinterpret_cast<float4*>(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + 4 * p), v);
+        }
+      } else {
+        const int total = nt * span;
+        for (int i = tid; i < total; i += kThreads) {
+          const int tr = i / span, p = i - tr * span;
+          st_cs(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + p, st[tr * RS + p]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  set_status(g.status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int pick_bt(int B, int T) {
+  int bt = 16;
+  while (bt > 1 && (B + bt - 1) / bt < 148) bt >>= 1;
+  while (bt > 1 && T * bt > kMaxTB) bt >>= 1;
+  return bt;
+}
+
+template <int BT, bool VEC, int MODE>
+static int launch_bt(const VtArgs& a, cudaStream_t s) {
+  const SmemPlan plan = make_plan(MODE, BT, a.T, a.A);
+  auto kern = vtrace_kernel<BT, VEC, MODE>;
+  if (plan.bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)plan.bytes);
+    if (e != cudaSuccess) {
+      set_error("vtrace: smem attribute (%zu bytes): %s", plan.bytes, cudaGetErrorString(e));
+      return BP_ERR_LAUNCH;
+    }
+  }
+  const int grid = (a.B + BT - 1) / BT;
+  kern<<<grid, kThreads, plan.bytes, s>>>(a);
+  return check_launch("vtrace_kernel");
+}
+
+template <int MODE>
+static int launch_mode(const VtArgs& a, cudaStream_t s, bool vec_ok) {
+  const int bt = pick_bt(a.B, a.T);
+  const bool vec = vec_ok && ((bt * a.A) % 4 == 0) && ((a.B * a.A) % 4 == 0);
+#define BP_VT_CASE(N)                                               \
+  case N:                                                           \
+    return vec ? launch_bt<N, true, MODE>(a, s) : launch_bt<N, false, MODE>(a, s);
+  switch (bt) {
+    BP_VT_CASE(16)
+    BP_VT_CASE(8)
+    BP_VT_CASE(4)
+    BP_VT_CASE(2)
+    BP_VT_CASE(1)
+  }
+#undef BP_VT_CASE
+  return BP_ERR_UNSUPPORTED;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static int check_dims(int T, int B, int A, bool need_a) {
+  if (T < 1 || B < 1 || (need_a && A < 1)) {
+    set_error("vtrace: bad dims T=%d B=%d A=%d", T, B, A);
+    return BP_ERR_ARG;
+  }
+  if (need_a && A > kMaxA) {
+    set_error("vtrace: num_actions %d > %d unsupported", A, kMaxA);
+    return BP_ERR_UNSUPPORTED;
+  }
+  if (T > kMaxTB) {
+    set_error("vtrace: unroll length %d > %d unsupported", T, kMaxTB);
+    return BP_ERR_UNSUPPORTED;
+  }
+  return BP_OK;
+}
+
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" int bp_vtrace_from_logits_f32(const float* behavior_logits, const float* target_logits,
+                                         const int64_t* actions, const float* discounts,
+                                         const float* rewards, const float* values,
+                                         const float* bootstrap_value, int T, int B, int A,
+                                         float clip_rho, float clip_pg_rho, float clip_c,
+                                         float* vs, float* pg_advantages, float* log_rhos,
+                                         float* behavior_logp, float* target_logp,
+                                         unsigned* status, void* stream) {
+  if (int e = check_dims(T, B, A, true)) return e;
+  if (!(clip_rho > 0.f && clip_pg_rho > 0.f && clip_c > 0.f)) {
+    set_error("vtrace: clip thresholds must be > 0");
+    return BP_ERR_ARG;
+  }
+  VtArgs a{};
+  a.beh = behavior_logits;
+  a.tgt = target_logits;
+  a.act = actions;
+  a.disc = discounts;
+  a.rew = rewards;
+  a.val = values;
+  a.boot = bootstrap_value;
+  a.T = T;
+  a.B = B;
+  a.A = A;
+  a.clip_rho = clip_rho;
+  a.clip_pg_rho = clip_pg_rho;
+  a.clip_c = clip_c;
+  a.vs = vs;
+  a.pg = pg_advantages;
+  a.log_rhos = log_rhos;
+  a.beh_logp = behavior_logp;
+  a.tgt_logp = target_logp;
+  a.status = status;
+  return launch_mode<MODE_LOGITS>(a, (cudaStream_t)stream,
+                                  aligned16(behavior_logits) && aligned16(target_logits));
+}
+
+extern "C" int bp_vtrace_from_importance_weights_f32(const float* log_rhos, const float* discounts,
+                                                     const float* rewards, const float* values,
+                                                     const float* bootstrap_value, int T, int B,
+                                                     float clip_rho, float clip_pg_rho,
+                                                     float clip_c, float* vs, float* pg_advantages,
+                                                     float* clipped_rhos, unsigned* status,
+                                                     void* stream) {
+  if (int e = check_dims(T, B, 1, false)) return e;
+  if (!(clip_rho > 0.f && clip_pg_rho > 0.f && clip_c > 0.f)) {
+    set_error("vtrace: clip thresholds must be > 0");
+    return BP_ERR_ARG;
+  }
+  VtArgs a{};
+  a.lr_in = log_rhos;
+  a.disc = discounts;
+  a.rew = rewards;
+  a.val = values;
+  a.boot = bootstrap_value;
+  a.T = T;
+  a.B = B;
+  a.A = 1;
+  a.clip_rho = clip_rho;
+  a.clip_pg_rho = clip_pg_rho;
+  a.clip_c = clip_c;
+  a.vs = vs;
+  a.pg = pg_advantages;
+  a.clipped_rhos = clipped_rhos;
+  a.status = status;
+  return launch_mode<MODE_IW>(a, (cudaStream_t)stream, false);
+}
+
+extern "C" size_t bp_learner_loss_workspace_bytes(int T, int B, int A) {
+  (void)A;
+  const int bt = pick_bt(B, T);
+  const size_t grid = (size_t)(B + bt - 1) / bt;
+  return 256 + grid * 3 * sizeof(double);
+}
+
+extern "C" int bp_learner_loss_f32(const float* learner_logits, const float* learner_baseline,
+                                   const float* behavior_logits, const int64_t* actions,
+                                   const float* rewards, const uint8_t* done, int T, int B, int A,
+                                   float discount, float clip_rho, float clip_pg_rho, float clip_c,
+                                   float pg_cost, float baseline_cost, float entropy_cost,
+                                   int reward_clip, float* d_logits, float* d_baseline, float* vs,
+                                   float* pg_advantages, double* losses, void* workspace,
+                                   unsigned* status, void* stream) {
+  if (int e = check_dims(T, B, A, true)) return e;
+  if (!(clip_rho > 0.f && clip_pg_rho > 0.f && clip_c > 0.f) || !(discount > 0.f && discount <= 1.f)) {
+    set_error("learner_loss: bad config (discount %g, clips %g %g %g)", discount, clip_rho,
+              clip_pg_rho, clip_c);
+    return BP_ERR_ARG;
+  }
+  if (!d_logits || !d_baseline || !losses || !workspace) {
+    set_error("learner_loss: null output/workspace");
+    return BP_ERR_ARG;
+  }
+  VtArgs a{};
+  a.beh = behavior_logits;
+  a.tgt = learner_logits;
+  a.act = actions;
+  a.done = done;
+  a.rew = rewards;
+  a.val = learner_baseline;
+  a.boot = learner_baseline + (size_t)T * B;
+  a.T = T;
+  a.B = B;
+  a.A = A;
+  a.clip_rho = clip_rho;
+  a.clip_pg_rho = clip_pg_rho;
+  a.clip_c = clip_c;
+  a.discount = discount;
+  a.pg_cost = pg_cost;
+  a.baseline_cost = baseline_cost;
+  a.entropy_cost = entropy_cost;
+  a.reward_clip = reward_clip;
+  a.vs = vs;
+  a.pg = pg_advantages;
+  a.d_logits = d_logits;
+  a.d_baseline = d_baseline;
+  a.losses = losses;
+  a.counter = reinterpret_cast<unsigned*>(workspace);
+  a.partials = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + 256);
+  a.status = status;
+  const bool vec = aligned16(learner_logits) && aligned16(behavior_logits) && aligned16(d_logits);
+  return launch_mode<MODE_LOSS>(a, (cudaStream_t)stream, vec);
+}
