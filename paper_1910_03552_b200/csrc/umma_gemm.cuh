@@ -1,0 +1,292 @@
+// Persistent, warp-specialised tcgen05 GEMM for the AtariNet torso (sm_100a).
+//
+//   D[128 x BN tile] = sum_kb A_kb[128 x 64] * B_kb[BN x 64]^T   (bf16 in, f32 in TMEM)
+//
+// Warp roles (256 threads, 1 CTA / SM, grid = min(tiles, #SMs)):
+//   warp 0      TMA producer: per K-block one (or two) A boxes + B boxes -> smem ring
+//   warp 1      MMA issuer:   4 x tcgen05.mma (K=16) per 64-wide K-block, commit -> empty[s]
+//   warp 2      TMEM allocator (2 accumulator buffers of BN f32 columns)
+//   warps 4..7  epilogue:     tcgen05.ld 32 columns at a time, fused bias / relu /
+//                             relu-mask / layout remap, vector stores
+// The accumulator is double buffered so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
+//
+// Operand addressing generalises "shifted GEMM" convolution: K-block kb of A
+// is a TMA box of the activation matrix [rows, C] at row offset off[kb / cb]
+// (one offset per filter tap), so stride-1 convolutions (and strided ones
+// after space-to-depth) need no im2col buffer.  For weight gradients the
+// reduction runs over rows and both operands are MN-major boxes.
+#pragma once
+#include "sm100.cuh"
+
+namespace bp {
+
+constexpr int kGemmThreads = 256;
+constexpr int kMaxShifts = 16;
+
+enum AMode { A_KMAJOR = 0, A_MNMAJOR = 1 };
+enum BMode { B_KMAJOR = 0, B_MNMAJOR = 1 };
+
+struct GemmArgs {
+  // tiling
+  int m_tiles, n_tiles, splits;
+  int num_kb;        // K blocks in total (K / 64 for K-major, rows / 64 for MN-major)
+  int kb_per_split;  // K blocks per split
+  // A operand
+  int a_cb;                    // K-major: 64-wide channel blocks per shift
+  int a_atoms_per_shift;       // MN-major: 64-wide M atoms per shift
+  int a_nshifts;               // MN-major: number of shifts (atoms beyond are zero)
+  int a_row_off[kMaxShifts];   // per-shift row offset (signed)
+  // B operand: K-major -> box (kb*64, n0); MN-major -> box (n0 + 64 j, kb*64)
+  // epilogue
+  int N;                 // full N (row-major ld of mask source / plain output)
+  int M;                 // valid M rows (rows >= M are not stored)
+  const float* bias;     // [N] or null
+  int relu;              // apply max(0, .)
+  const __nv_bfloat16* mask;  // relu-backward mask source, same (m, n) index, ld N; null = none
+  int out_f32;           // 1: f32 output, 0: bf16
+  void* out;
+  long long split_stride;  // elements between split partial outputs
+  // row map: m -> (img, y, x) on a gh x gw grid; valid iff y < vh && x < vw
+  int gh, gw, vh, vw, sy, sx;
+  long long r_img, r_y, r_x, r_sub;
+  // column map: C(n) = ((n/cdiv)/cq)*cs1 + ((n/cdiv)%cq)*cs2 + n%cdiv
+  int cdiv, cq;
+  long long cs1, cs2;
+};
+
+template <int BN, int AM, int BM, int BSWZ>
+struct GemmCfg {
+  static constexpr uint32_t A_BYTES = 128 * 64 * 2;
+  static constexpr uint32_t B_BYTES = BN * 64 * 2;
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  static_assert(BM == B_KMAJOR || BSWZ == 128 || (BSWZ == 64 && BN == 32), "B swizzle");
+};
+
+BP_DEVICE void tile_coords(const GemmArgs& g, int tile, int& mt, int& nt, int& sp) {
+  sp = tile % g.splits;
+  const int r = tile / g.splits;
+  nt = r % g.n_tiles;
+  mt = r / g.n_tiles;
+}
+
+template <int BN, int AM, int BM, int BSWZ>
+BP_DEVICE void issue_loads(const GemmArgs& g, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                           int mt, int nt, int kb, uint8_t* sa, uint8_t* sb, uint64_t* bar) {
+  if constexpr (AM == A_KMAJOR) {
+    const int s = kb / g.a_cb;
+    const int cb = kb - s * g.a_cb;
+    sm100::tma_load_2d(sa, tmA, bar, cb * 64, mt * 128 + g.a_row_off[s]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int atom = mt * 2 + j;
+      const int s = atom / g.a_atoms_per_shift;
+      const int cb = atom - s * g.a_atoms_per_shift;
+      // shifts beyond the last are all-zero atoms: point the box fully out of bounds
+      const int y = (s < g.a_nshifts) ? kb * 64 + g.a_row_off[s] : 0x3fffffff;
+      sm100::tma_load_2d(sa + j * 8192, tmA, bar, cb * 64, y);
+    }
+  }
+  if constexpr (BM == B_KMAJOR) {
+    sm100::tma_load_2d(sb, tmB, bar, kb * 64, nt * BN);
+  } else if constexpr (BSWZ == 64) {
+    sm100::tma_load_2d(sb, tmB, bar, nt * BN, kb * 64);
+  } else {
+#pragma unroll
+    for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, tmB, bar, nt * BN + j * 64, kb * 64);
+  }
+}
+
+template <int AM>
+BP_DEVICE uint64_t a_desc(uint32_t base, int k) {
+  if constexpr (AM == A_KMAJOR) return sm100::smem_desc(base + k * 32, 16, 1024, sm100::SWZ_128B);
+  else return sm100::smem_desc(base + k * 2048, 8192, 1024, sm100::SWZ_128B);
+}
+template <int BM, int BSWZ>
+BP_DEVICE uint64_t b_desc(uint32_t base, int k) {
+  if constexpr (BM == B_KMAJOR) return sm100::smem_desc(base + k * 32, 16, 1024, sm100::SWZ_128B);
+  else if constexpr (BSWZ == 64) return sm100::smem_desc(base + k * 1024, 16, 512, sm100::SWZ_64B);
+  else return sm100::smem_desc(base + k * 2048, 8192, 1024, sm100::SWZ_128B);
+}
+
+BP_DEVICE uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// one row x 32 consecutive columns of the tile
+BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
+                              int sp, float (&v)[32]) {
+  if (!row_ok) return;
+  if (g.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += __ldg(g.bias + n0 + i);
+  }
+  if (g.relu) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  if (g.mask) {
+    const uint4* mp = reinterpret_cast<const uint4*>(g.mask + (size_t)m * g.N + n0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 w = __ldg(mp + q);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (!(__bfloat162float(h[i]) > 0.f)) v[q * 8 + i] = 0.f;
+    }
+  }
+  const int qd = n0 / g.cdiv;
+  const long long cbase = (long long)(qd / g.cq) * g.cs1 + (long long)(qd % g.cq) * g.cs2 + (n0 % g.cdiv);
+  const long long off = rbase + cbase + (long long)sp * g.split_stride;
+  if (g.out_f32) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out) + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                        pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+  }
+}
+
+template <int BN, int AM, int BM, int BSWZ>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    umma_gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB) {
+  using C = GemmCfg<BN, AM, BM, BSWZ>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 4);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int ntiles = g.m_tiles * g.n_tiles * g.splits;
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int mt, nt, sp;
+        tile_coords(g, tile, mt, nt, sp);
+        const int kb0 = sp * g.kb_per_split;
+        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE);
+          uint8_t* sa = smem + stage * C::STAGE;
+          issue_loads<BN, AM, BM, BSWZ>(g, &tmA, &tmB, mt, nt, kb, sa, sa + C::A_BYTES, &full[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(128, BN, AM == A_MNMAJOR, BM == B_MNMAJOR);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int mt, nt, sp;
+        tile_coords(g, tile, mt, nt, sp);
+        const int kb0 = sp * g.kb_per_split;
+        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        sm100::mbar_wait(&tempty[acc], aphase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            sm100::umma_f16(d, a_desc<AM>(sa, k), b_desc<BM, BSWZ>(sb, k), idesc,
+                            (kb > kb0 || k > 0) ? 1u : 0u);
+          sm100::umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (kb1 <= kb0) {
+          // empty split: nothing accumulated; still hand the (zero) tile over
+        }
+        sm100::umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int mt, nt, sp;
+      tile_coords(g, tile, mt, nt, sp);
+      const int m = mt * 128 + ew * 32 + lane;
+      // row map
+      bool row_ok = m < g.M;
+      long long rbase = 0;
+      {
+        const int per = g.gh * g.gw;
+        const int img = m / per;
+        const int rem = m - img * per;
+        const int y = rem / g.gw;
+        const int x = rem - y * g.gw;
+        row_ok = row_ok && (y < g.vh) && (x < g.vw);
+        rbase = (long long)img * g.r_img + (long long)(y / g.sy) * g.r_y + (long long)(x / g.sx) * g.r_x +
+                (long long)((y % g.sy) * g.sx + (x % g.sx)) * g.r_sub;
+      }
+      sm100::mbar_wait(&tfull[acc], aphase);
+      sm100::tc_fence_after();
+      const bool has_k = (sp * g.kb_per_split) < g.num_kb;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(r[i]) : 0.f;
+        epilogue_chunk(g, rbase, row_ok, m, nt * BN + c, sp, v);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace bp

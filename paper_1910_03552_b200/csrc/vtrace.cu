@@ -11,16 +11,19 @@
 // columns for ALL T rows (columns are independent; the scan runs along T).
 //
 //   phase 1  row-parallel, streamed over T in chunks of TC = 128/BT time rows:
-//            cp.async (LDGSTS) 3-stage ring brings the (TC, BT*A) logits spans
-//            (contiguous per time row) into shared memory; one thread per
-//            (t, b) row computes both log-softmaxes, gathers the action, and
-//            parks log_rho / discount / reward / value in smem scan arrays.
+//            warp 0 issues one TMA bulk copy (cp.async.bulk + mbarrier) per
+//            contiguous (time row, BT*A) logits span into a 2-4 stage smem ring
+//            (cp.async fallback when spans are not 16B multiples); one thread
+//            per (t, b) row computes both log-softmaxes (row in registers for
+//            A = 6 / 18), gathers the action, and parks log_rho / discount /
+//            reward / value in smem scan arrays.
 //   phase 2  parallel delta / c precompute, then the serial reverse scan
 //            acc = delta_t + gamma_t c_t acc (BT threads, FMA chain only),
 //            then parallel vs / pg_advantage outputs.
 //   phase 3  (MODE_LOSS) loss partial sums -> deterministic last-block reduce;
-//            second streamed pass over the learner logits (L2-resident) writes
-//            d_logits through smem with coalesced vector stores.
+//            second streamed pass over the learner logits (L2-resident, already
+//            prefetched under phase 2) computes d_logits in smem and writes them
+//            back with TMA bulk stores.
 #include <cstdio>
 #include <cstdarg>
 #include <algorithm>
@@ -31,10 +34,12 @@ namespace bp {
 
 enum { MODE_LOGITS = 0, MODE_IW = 1, MODE_LOSS = 2 };
 
-constexpr int kThreads = 128;  // == rows per chunk
-constexpr int kStages = 3;
+constexpr int kThreads = 128;  // == (t, b) rows per chunk
+constexpr int kMaxStages = 4;
+constexpr int kCpAsyncStages = 3;
 constexpr int kMaxA = 48;
 constexpr int kMaxTB = 2048;  // T * BT bound for the smem scan arrays
+constexpr size_t kSmemBudget = 100 * 1024;  // -> 2 CTAs / SM
 
 struct VtArgs {
   const float* beh;      // (T,B,A)
@@ -67,30 +72,37 @@ struct VtArgs {
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
 
 struct SmemPlan {
-  int TC, RS;            // time rows per chunk, smem row stride (floats)
+  int TC, RS, nst;       // time rows per chunk, smem row stride (floats), pipeline stages
   size_t stage_floats;   // per stage, both tensors
   size_t scan_off;       // float offset of the scan arrays
   int n_scan;            // number of T*BT arrays
   size_t bytes;
 };
 
-__host__ __device__ inline SmemPlan make_plan(int mode, int BT, int T, int A) {
+__host__ __device__ inline SmemPlan make_plan(int mode, int BT, int T, int A, bool bulk) {
   SmemPlan p;
   p.TC = kThreads / BT;
   p.RS = round_up4(BT * A);
   const int ntens = (mode == MODE_IW) ? 0 : 2;
   p.stage_floats = (size_t)ntens * p.TC * p.RS;
-  p.scan_off = p.stage_floats * kStages;
   p.n_scan = (mode == MODE_LOSS) ? 10 : 6;
-  p.bytes = (p.scan_off + (size_t)p.n_scan * T * BT + BT) * sizeof(float);
+  const size_t scan_floats = (size_t)p.n_scan * T * BT + BT;
+  if (bulk) {
+    p.nst = kMaxStages;
+    while (p.nst > 2 && (p.nst * p.stage_floats + scan_floats) * sizeof(float) > kSmemBudget) --p.nst;
+  } else {
+    p.nst = kCpAsyncStages;
+  }
+  p.scan_off = p.nst * p.stage_floats;
+  p.bytes = (p.scan_off + scan_floats) * sizeof(float);
   return p;
 }
 
-// issue the cp.async copies of logits chunk c (time rows t0..t0+nt) into a stage
-template <int BT, bool VEC>
-BP_DEVICE void issue_chunk(float* stage, const float* src, int RS, int t0, int nt, int b0,
-                           int bw, int B, int A) {
-  const int span = bw * A;  // floats per time row (contiguous in global)
+// cp.async fallback (unaligned spans / tiny tiles): all threads copy 4 or 16 bytes each
+template <bool VEC>
+BP_DEVICE void issue_chunk_cpasync(float* stage, const float* src, int RS, int t0, int nt, int b0,
+                                   int bw, int B, int A) {
+  const int span = bw * A;
   if constexpr (VEC) {
     const int pieces = span >> 2;
     const int total = nt * pieces;
@@ -110,28 +122,56 @@ BP_DEVICE void issue_chunk(float* stage, const float* src, int RS, int t0, int n
 }
 
 struct RowSoftmax {
-  float lse;     // log sum exp (max-shifted form: m + log s)
+  float lse;     // log sum exp (max-shifted: m + log s)
   float xa;      // logit of the action
   float ent;     // entropy (only when requested)
   bool finite;
 };
 
-template <bool ENT>
+// log-softmax statistics of one row x[0..A); AT > 0: A known at compile time
+// (row held in registers, vector LDS), AT == 0: runtime A.
+template <int AT, bool ENT>
 BP_DEVICE RowSoftmax row_softmax(const float* x, int A, int a) {
-  float m = -INFINITY, sx = 0.f;
-  for (int j = 0; j < A; ++j) {
-    const float v = x[j];
-    m = fmaxf(m, v);
-    sx += v;
-  }
-  float s = 0.f, sxe = 0.f;
-  for (int j = 0; j < A; ++j) {
-    const float z = x[j] - m;
-    const float e = fast_exp(z);
-    s += e;
-    if constexpr (ENT) sxe += e * z;
-  }
   RowSoftmax r;
+  float m = -INFINITY, sx = 0.f, s = 0.f, sxe = 0.f;
+  if constexpr (AT > 0) {
+    float v[AT];
+    if constexpr (AT % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < AT / 2; ++i) {
+        const float2 t = reinterpret_cast<const float2*>(x)[i];
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < AT; ++i) v[i] = x[i];
+    }
+#pragma unroll
+    for (int i = 0; i < AT; ++i) {
+      m = fmaxf(m, v[i]);
+      sx += v[i];
+    }
+#pragma unroll
+    for (int i = 0; i < AT; ++i) {
+      const float z = v[i] - m;
+      const float e = fast_exp(z);
+      s += e;
+      if constexpr (ENT) sxe = fmaf(e, z, sxe);
+    }
+  } else {
+    for (int j = 0; j < A; ++j) {
+      const float v = x[j];
+      m = fmaxf(m, v);
+      sx += v;
+    }
+    for (int j = 0; j < A; ++j) {
+      const float z = x[j] - m;
+      const float e = fast_exp(z);
+      s += e;
+      if constexpr (ENT) sxe = fmaf(e, z, sxe);
+    }
+  }
   const float ls = fast_log(s);
   r.lse = m + ls;
   r.xa = x[a];
@@ -140,17 +180,37 @@ BP_DEVICE RowSoftmax row_softmax(const float* x, int A, int a) {
   return r;
 }
 
-template <int BT, bool VEC, int MODE>
+template <int AT>
+BP_DEVICE void dlogits_row(float* x, int A, int a, float lse, float H, float pa, float ec) {
+  // d = pg_cost*adv*(pi - onehot) + ent_cost*pi*(log pi + H)   (vtrace.py:207-210)
+  if constexpr (AT > 0) {
+#pragma unroll
+    for (int j = 0; j < AT; ++j) {
+      const float lp = x[j] - lse;
+      const float p = fast_exp(lp);
+      x[j] = pa * (p - (j == a ? 1.f : 0.f)) + ec * p * (lp + H);
+    }
+  } else {
+    for (int j = 0; j < A; ++j) {
+      const float lp = x[j] - lse;
+      const float p = fast_exp(lp);
+      x[j] = pa * (p - (j == a ? 1.f : 0.f)) + ec * p * (lp + H);
+    }
+  }
+}
+
+template <int BT, bool BULK, bool VEC, int MODE, int AT>
 __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
-  extern __shared__ __align__(16) float smem[];
-  const int T = g.T, B = g.B, A = g.A;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  const int T = g.T, B = g.B, A = (AT > 0) ? AT : g.A;
   const int b0 = blockIdx.x * BT;
   const int bw = min(BT, B - b0);
-  const SmemPlan plan = make_plan(MODE, BT, T, A);
-  const int TC = plan.TC, RS = plan.RS;
+  const SmemPlan plan = make_plan(MODE, BT, T, A, BULK);
+  const int TC = plan.TC, RS = plan.RS, nst = plan.nst;
   const int TB = T * BT;
   float* scan = smem + plan.scan_off;
-  float* s_lr = scan;            // log_rho -> pg rho clip
+  float* s_lr = scan;              // log_rho -> pg rho clip
   float* s_disc = scan + TB;
   float* s_rew = scan + 2 * TB;
   float* s_val = scan + 3 * TB;
@@ -163,34 +223,76 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
   float* s_boot = scan + plan.n_scan * TB;
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int tl = tid / BT;  // time row within chunk
   const int bl = tid % BT;  // column within tile
+  const uint32_t span_bytes = (uint32_t)(bw * A * sizeof(float));
   unsigned bad = 0;
 
-  if (tid < BT && tid < bw) {
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < nst; ++s) mbar_init(&full_bar[s], 1);
+      fence_mbar_init();
+    }
+  }
+  if (tid < bw) {
     const float bv = g.boot[b0 + tid];
     s_boot[tid] = bv;
     if (!isfinite(bv)) bad |= BP_STATUS_NONFINITE_IN;
   }
+  __syncthreads();
 
-  // ----------------------------------------------------------------- phase 1
   const int nchunks = (T + TC - 1) / TC;
-  if constexpr (MODE != MODE_IW) {
-    const float* tens[2] = {g.beh, g.tgt};
-    auto issue = [&](int c) {
-      if (c < nchunks) {
-        float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+  // chunk q < nchunks: phase-1 logits (beh + tgt); q >= nchunks: phase-3 learner logits
+  auto issue = [&](int q) {
+    const bool p3 = q >= nchunks;
+    const int c = p3 ? q - nchunks : q;
+    if constexpr (BULK) {
+      if (warp == 0 && c < nchunks && (!p3 || MODE == MODE_LOSS)) {
+        float* st = smem + (size_t)(q % nst) * plan.stage_floats;
         const int t0 = c * TC, nt = min(TC, T - t0);
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-          issue_chunk<BT, VEC>(st + k * TC * RS, tens[k], RS, t0, nt, b0, bw, B, A);
+        const int ntens = p3 ? 1 : 2;
+        if (p3) {
+          bulk_wait_read_all();  // this stage may still be feeding d_logits bulk stores
+          __syncwarp();
+        }
+        if (lane == 0) mbar_expect_tx(&full_bar[q % nst], span_bytes * nt * ntens);
+        __syncwarp();
+        for (int r = lane; r < nt * ntens; r += 32) {
+          const int k = r / nt, tr = r - k * nt;
+          const float* src = (p3 || k == 1) ? g.tgt : g.beh;
+          bulk_g2s(st + k * TC * RS + tr * RS, src + ((size_t)(t0 + tr) * B + b0) * A, span_bytes,
+                   &full_bar[q % nst]);
+        }
+      }
+    } else {
+      if (c < nchunks && (!p3 || MODE == MODE_LOSS)) {
+        float* st = smem + (size_t)(q % nst) * plan.stage_floats;
+        const int t0 = c * TC, nt = min(TC, T - t0);
+        if (p3) {
+          issue_chunk_cpasync<VEC>(st, g.tgt, RS, t0, nt, b0, bw, B, A);
+        } else {
+          issue_chunk_cpasync<VEC>(st, g.beh, RS, t0, nt, b0, bw, B, A);
+          issue_chunk_cpasync<VEC>(st + TC * RS, g.tgt, RS, t0, nt, b0, bw, B, A);
+        }
       }
       cp_async_commit();
-    };
-#pragma unroll
-    for (int c = 0; c < kStages - 1; ++c) issue(c);
+    }
+  };
+  auto wait_chunk = [&](int q) {
+    if constexpr (BULK) {
+      mbar_wait_parity(&full_bar[q % nst], (uint32_t)((q / nst) & 1));
+    } else {
+      cp_async_wait<kCpAsyncStages - 1>();
+      __syncthreads();
+    }
+  };
+
+  // ----------------------------------------------------------------- phase 1
+  if constexpr (MODE != MODE_IW) {
+    for (int q = 0; q < nst - 1; ++q) issue(q);
     for (int c = 0; c < nchunks; ++c) {
-      issue(c + kStages - 1);
+      issue(c + nst - 1);
       const int t = c * TC + tl;
       const bool live = (t < T) && (bl < bw);
       // small per-row inputs: plain loads issued before the wait
@@ -199,23 +301,22 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
       uint8_t dn = 0;
       const size_t idx = (size_t)t * B + b0 + bl;
       if (live) {
-        a64 = g.act[idx];
-        rv = g.rew[idx];
-        vv = g.val[idx];
-        if constexpr (MODE == MODE_LOSS) dn = g.done[idx];
-        else dv = g.disc[idx];
+        a64 = __ldg(g.act + idx);
+        rv = __ldg(g.rew + idx);
+        vv = __ldg(g.val + idx);
+        if constexpr (MODE == MODE_LOSS) dn = __ldg(g.done + idx);
+        else dv = __ldg(g.disc + idx);
       }
-      cp_async_wait<kStages - 1>();
-      __syncthreads();
+      wait_chunk(c);
       if (live) {
-        const float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+        const float* st = smem + (size_t)(c % nst) * plan.stage_floats;
         int a = (int)a64;
         if (a64 < 0 || a64 >= A) {
           bad |= BP_STATUS_ACTION_RANGE;
           a = 0;
         }
-        const RowSoftmax rb = row_softmax<false>(st + tl * RS + bl * A, A, a);
-        const RowSoftmax rt = row_softmax<MODE == MODE_LOSS>(st + TC * RS + tl * RS + bl * A, A, a);
+        const RowSoftmax rb = row_softmax<AT, false>(st + tl * RS + bl * A, A, a);
+        const RowSoftmax rt = row_softmax<AT, MODE == MODE_LOSS>(st + TC * RS + tl * RS + bl * A, A, a);
         const float blp = rb.xa - rb.lse;
         const float tlp = rt.xa - rt.lse;
         const float lr = tlp - blp;
@@ -227,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         }
         if (!(rb.finite && rt.finite && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(dv)))
           bad |= BP_STATUS_NONFINITE_IN;
-        const int si = tl * BT + bl + c * TC * BT;  // == t*BT + bl
+        const int si = t * BT + bl;
         s_lr[si] = lr;
         s_disc[si] = dv;
         s_rew[si] = rv;
@@ -243,8 +344,10 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
           if (g.tgt_logp) g.tgt_logp[idx] = tlp;
         }
       }
-      __syncthreads();  // stage (c % kStages) may be refilled next iteration
+      __syncthreads();  // stage (c % nst) may be refilled next iteration
     }
+    // (in MODE_LOSS the loop tail above already issued the first nst-1 phase-3
+    //  chunks of learner logits, so they stream in under phase 2)
   } else {
     // MODE_IW: only (T,B) inputs -- straight coalesced loads into smem
     for (int i = tid; i < TB; i += kThreads) {
@@ -261,8 +364,8 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         s_val[i] = vv;
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
 
   // ----------------------------------------------------------------- phase 2
   // 2a: delta_t = min(rho_bar, rho)(r + gamma V_{t+1} - V), gamma*c  (vtrace.py:113-117)
@@ -287,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
   if (tid < bw) {
     float acc = 0.f;
     int i = (T - 1) * BT + tid;
-#pragma unroll 4
+#pragma unroll 8
     for (int t = T - 1; t >= 0; --t, i -= BT) {
       acc = fmaf(s_dc[i], acc, s_delta[i]);
       s_delta[i] = acc;
@@ -316,24 +419,21 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
       }
     }
   }
-  if constexpr (MODE == MODE_LOSS) {
-    if (tid < bw) g.d_baseline[(size_t)T * B + b0 + tid] = 0.f;  // bootstrap row: stop-grad
-  }
 
   if constexpr (MODE == MODE_LOSS) {
+    if (tid < bw) g.d_baseline[(size_t)T * B + b0 + tid] = 0.f;  // bootstrap row: stop-grad
     // ------------------------------------------------------- phase 3a: loss sums
     __shared__ double red[3][kThreads / 32];
+    __shared__ bool is_last;
     pg_sum = warp_sum(pg_sum);
     base_sum = warp_sum(base_sum);
     ent_sum = warp_sum(ent_sum);
-    const int w = tid >> 5, l = tid & 31;
-    if (l == 0) {
-      red[0][w] = pg_sum;
-      red[1][w] = base_sum;
-      red[2][w] = ent_sum;
+    if (lane == 0) {
+      red[0][warp] = pg_sum;
+      red[1][warp] = base_sum;
+      red[2][warp] = ent_sum;
     }
     __syncthreads();  // also orders s_dc (pg advantages) for phase 3b
-    __shared__ bool is_last;
     if (tid == 0) {
       double a0 = 0, a1 = 0, a2 = 0;
       for (int k = 0; k < kThreads / 32; ++k) {
@@ -368,54 +468,48 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
     }
 
     // ------------------------------------------------------- phase 3b: d_logits
-    // d = pg_cost*adv*(pi - onehot) + ent_cost*pi*(log pi + H)   (vtrace.py:207-210)
-    auto issue = [&](int c) {
-      if (c < nchunks) {
-        float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
-        const int t0 = c * TC, nt = min(TC, T - t0);
-        issue_chunk<BT, VEC>(st, g.tgt, RS, t0, nt, b0, bw, B, A);
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int c = 0; c < kStages - 1; ++c) issue(c);
     for (int c = 0; c < nchunks; ++c) {
-      issue(c + kStages - 1);
-      cp_async_wait<kStages - 1>();
-      __syncthreads();
-      float* st = smem + (size_t)(c % kStages) * plan.stage_floats;
+      const int q = nchunks + c;
+      issue(q + nst - 1);
+      wait_chunk(q);
+      float* st = smem + (size_t)(q % nst) * plan.stage_floats;
       const int t0 = c * TC, nt = min(TC, T - t0);
       const int t = t0 + tl;
       if (t < T && bl < bw) {
         const int si = t * BT + bl;
-        const float lse = s_lse[si], H = s_ent[si], adv = s_dc[si];
-        const int a = s_act[si];
-        float* x = st + tl * RS + bl * A;
-        const float pa = g.pg_cost * adv, ec = g.entropy_cost;
-        for (int j = 0; j < A; ++j) {
-          const float lp = x[j] - lse;
-          const float p = fast_exp(lp);
-          x[j] = pa * (p - (j == a ? 1.f : 0.f)) + ec * p * (lp + H);
-        }
+        dlogits_row<AT>(st + tl * RS + bl * A, A, s_act[si], s_lse[si], s_ent[si],
+                        g.pg_cost * s_dc[si], g.entropy_cost);
       }
-      __syncthreads();
-      // coalesced copy-out of the chunk
-      const int span = bw * A;
-      if constexpr (VEC) {
-        const int pieces = span >> 2, total = nt * pieces;
-        for (int i = tid; i < total; i += kThreads) {
-          const int tr = i / pieces, p = i - tr * pieces;
-          const float4 v = *reinterpret_cast<const float4*>(st + tr * RS + 4 * p);
-          st_cs4(reinterpret_cast<float4*>(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + 4 * p), v);
+      if constexpr (BULK) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (warp == 0) {
+          for (int r = lane; r < nt; r += 32)
+            bulk_s2g(g.d_logits + ((size_t)(t0 + r) * B + b0) * A, st + r * RS, span_bytes);
+          bulk_commit();
         }
       } else {
-        const int total = nt * span;
-        for (int i = tid; i < total; i += kThreads) {
-          const int tr = i / span, p = i - tr * span;
-          st_cs(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + p, st[tr * RS + p]);
+        __syncthreads();
+        const int span = bw * A;
+        if constexpr (VEC) {
+          const int pieces = span >> 2, total = nt * pieces;
+          for (int i = tid; i < total; i += kThreads) {
+            const int tr = i / pieces, p = i - tr * pieces;
+            const float4 v = *reinterpret_cast<const float4*>(st + tr * RS + 4 * p);
+            st_cs4(reinterpret_cast<float4*>(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + 4 * p), v);
+          }
+        } else {
+          const int total = nt * span;
+          for (int i = tid; i < total; i += kThreads) {
+            const int tr = i / span, p = i - tr * span;
+            st_cs(g.d_logits + ((size_t)(t0 + tr) * B + b0) * A + p, st[tr * RS + p]);
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
+    }
+    if constexpr (BULK) {
+      if (warp == 0) bulk_wait_all();
     }
   }
   set_status(g.status, bad);
@@ -426,15 +520,16 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
 // ---------------------------------------------------------------------------
 static int pick_bt(int B, int T) {
   int bt = 16;
-  while (bt > 1 && (B + bt - 1) / bt < 148) bt >>= 1;
+  while (bt > 1 && (B + bt - 1) / bt < 2 * 148) bt >>= 1;
+  if (bt == 2) bt = 1;
   while (bt > 1 && T * bt > kMaxTB) bt >>= 1;
   return bt;
 }
 
-template <int BT, bool VEC, int MODE>
-static int launch_bt(const VtArgs& a, cudaStream_t s) {
-  const SmemPlan plan = make_plan(MODE, BT, a.T, a.A);
-  auto kern = vtrace_kernel<BT, VEC, MODE>;
+template <int BT, bool BULK, bool VEC, int MODE, int AT>
+static int launch_cfg(const VtArgs& a, cudaStream_t s) {
+  const SmemPlan plan = make_plan(MODE, BT, a.T, a.A, BULK);
+  auto kern = vtrace_kernel<BT, BULK, VEC, MODE, AT>;
   if (plan.bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)plan.bytes);
@@ -448,21 +543,31 @@ static int launch_bt(const VtArgs& a, cudaStream_t s) {
   return check_launch("vtrace_kernel");
 }
 
+template <int BT, int MODE, int AT>
+static int launch_path(const VtArgs& a, cudaStream_t s, bool vec_ok) {
+  // bulk (TMA 1D) path: every per-time-row span is 16B aligned and a multiple of 16 bytes
+  const bool spans16 = ((BT * a.A) % 4 == 0) && ((a.B * a.A) % 4 == 0);
+  if (MODE != MODE_IW && vec_ok && spans16) return launch_cfg<BT, true, true, MODE, AT>(a, s);
+  if (vec_ok && spans16) return launch_cfg<BT, false, true, MODE, AT>(a, s);
+  return launch_cfg<BT, false, false, MODE, AT>(a, s);
+}
+
+template <int BT, int MODE>
+static int launch_a(const VtArgs& a, cudaStream_t s, bool vec_ok) {
+  if (MODE == MODE_IW) return launch_path<BT, MODE, 1>(a, s, false);
+  if (a.A == 6) return launch_path<BT, MODE, 6>(a, s, vec_ok);
+  if (a.A == 18) return launch_path<BT, MODE, 18>(a, s, vec_ok);
+  return launch_path<BT, MODE, 0>(a, s, vec_ok);
+}
+
 template <int MODE>
 static int launch_mode(const VtArgs& a, cudaStream_t s, bool vec_ok) {
-  const int bt = pick_bt(a.B, a.T);
-  const bool vec = vec_ok && ((bt * a.A) % 4 == 0) && ((a.B * a.A) % 4 == 0);
-#define BP_VT_CASE(N)                                               \
-  case N:                                                           \
-    return vec ? launch_bt<N, true, MODE>(a, s) : launch_bt<N, false, MODE>(a, s);
-  switch (bt) {
-    BP_VT_CASE(16)
-    BP_VT_CASE(8)
-    BP_VT_CASE(4)
-    BP_VT_CASE(2)
-    BP_VT_CASE(1)
+  switch (pick_bt(a.B, a.T)) {
+    case 16: return launch_a<16, MODE>(a, s, vec_ok);
+    case 8: return launch_a<8, MODE>(a, s, vec_ok);
+    case 4: return launch_a<4, MODE>(a, s, vec_ok);
+    case 1: return launch_a<1, MODE>(a, s, vec_ok);
   }
-#undef BP_VT_CASE
   return BP_ERR_UNSUPPORTED;
 }
 
