@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Headline benchmark: IMPALA learner step (TorchBeast learn()) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): AtariNet (no LSTM) learner step, T=80,
+B=32 per GPU, 4x84x84 u8 synthetic frames, A=6, RMSprop + global-norm clip;
+N>1 GPUs: data-parallel over B (B=32 per rank, weak scaling) with an NCCL
+SUM all-reduce of the flat gradient buffer.
+
+metric  learner env-frames/s = T*B*N / step time.  `value`: inputs resident in
+        HBM, device time per step (CUDA events on the launching stream, L2
+        flushed before every timed step by a 256 MB memset outside the timed
+        window, max over ranks).  `e2e`: the same step through the public
+        `learn()` API with the batch copied from pinned host memory inside the
+        timed window and the loss stats read back.
+roofline  dominant kernel of the step, timed live with CUDA events.
+cpu_baseline  the CPU oracle port (torch-CPU restatement of upstream learn(),
+        oracle/atari_ref.py) on the host cores, bounded sample.
+--impl reference  that CPU port is the reference arm (the reference package is
+        pure numpy and has no AtariNet / GPU path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+T_UNROLL, B_PER_GPU, NUM_ACTIONS = 80, 32, 6
+FLAGS = dict(discounting=0.99, baseline_cost=0.5, entropy_cost=0.0006, reward_clipping="abs_one",
+             grad_norm_clipping=40.0, learning_rate=0.00048, alpha=0.99, epsilon=0.01, momentum=0.0)
+# algorithmic FLOPs of the AtariNet learner step per frame: forward 2*MACs,
+# backward = dgrad (all but conv1) + wgrad
+MACS = dict(conv1=400 * 32 * 256, conv2=81 * 64 * 512, conv3=49 * 64 * 576, fc=3136 * 512,
+            heads=512 * 7)
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                    kind="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, kind="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_batch(T, B, A, device, seed):
+    g = torch.Generator(device=device).manual_seed(seed)
+    t1 = T + 1
+    return dict(
+        frame=torch.randint(0, 256, (t1, B, 4, 84, 84), dtype=torch.uint8, device=device, generator=g),
+        reward=torch.rand(t1, B, device=device, generator=g) * 2 - 1,
+        done=torch.rand(t1, B, device=device, generator=g) < 0.05,
+        episode_return=torch.randn(t1, B, device=device, generator=g),
+        episode_step=torch.randint(0, 1000, (t1, B), device=device, generator=g),
+        policy_logits=torch.randn(t1, B, A, device=device, generator=g),
+        baseline=torch.randn(t1, B, device=device, generator=g),
+        last_action=torch.randint(0, A, (t1, B), device=device, generator=g),
+        action=torch.randint(0, A, (t1, B), device=device, generator=g),
+    )
+
+
+def cpu_reference(T, B, A, steps, warmup, budget_s=120.0):
+    """Time the CPU oracle port of upstream learn() (torch CPU, all host threads)."""
+    from oracle import atari_ref
+
+    nthreads = os.cpu_count() or 1
+    torch.set_num_threads(nthreads)
+    torch.manual_seed(0)
+    model = atari_ref.AtariNetRef(num_actions=A)
+    opt = torch.optim.RMSprop(model.parameters(), lr=FLAGS["learning_rate"], alpha=FLAGS["alpha"],
+                              eps=FLAGS["epsilon"])
+    batch = atari_ref.synthetic_batch(T, B, A, seed=0)
+    for _ in range(max(0, min(warmup, 1))):
+        atari_ref.learn_step(model, opt, batch, FLAGS)
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        atari_ref.learn_step(model, opt, batch, FLAGS)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    per = statistics.median(times)
+    return dict(value=T * B / per, unit="env-frames/s", cores=nthreads, kind="port",
+                sample=f"{len(times)} full learn() steps T={T} B={B} A={A} (torch-CPU restatement, "
+                       f"{nthreads} threads), median {per * 1e3:.1f} ms/step")
+
+
+def kernel_breakdown(L, batch, opt, iters=5):
+    """Per-phase device times of one step (CUDA events between launches), for the roofline."""
+    from paper_1910_03552_b200 import _native as N
+
+    m = L.model
+    T, B, n = L.T, L.B, L.n
+    s = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+    reward = batch["reward"]
+    la = batch["last_action"]
+    frames = batch["frame"].reshape(n, 4, 84, 84)
+    acc = {}
+    for _ in range(iters):
+        ev[0].record(s)
+        m.pack_weights()
+        ev[1].record(s)
+        N.check(N.lib().bp_atari_forward(m._bufs.ref, n, N.ptr(frames), N.ptr(reward.reshape(n)),
+                                         N.ptr(la.reshape(n)), N.ptr(m.flat_params), N.ptr(L.logits),
+                                         N.ptr(L.baseline), N.stream_handle()), "fwd")
+        ev[2].record(s)
+        A = m.num_actions
+        L.loss(L.logits[:T * B].view(T, B, A), L.baseline.view(T + 1, B), batch["policy_logits"][1:],
+               batch["action"][1:], reward[1:], batch["done"][1:], L.cfg,
+               d_logits=L.d_logits[:T * B].view(T, B, A), d_baseline=L.d_baseline.view(T + 1, B),
+               losses=L.losses)
+        ev[3].record(s)
+        m._backward_kernels(L.d_logits, L.d_baseline, reward.reshape(n), la.reshape(n), m.flat_grads)
+        ev[4].record(s)
+        opt.step(max_norm=L.max_norm)
+        ev[5].record(s)
+        torch.cuda.synchronize()
+        for name, (a, b) in dict(pack=(0, 1), forward=(1, 2), loss=(2, 3), backward=(3, 4),
+                                 optimizer=(4, 5)).items():
+            acc.setdefault(name, []).append(ev[a].elapsed_time(ev[b]) * 1e-3)
+    return {k: statistics.median(v) for k, v in acc.items()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    T, B, A = T_UNROLL, B_PER_GPU, NUM_ACTIONS
+    config = {"workload": "configs[1]: AtariNet (no LSTM) learner step + RMSprop", "T": T,
+              "B_per_gpu": B, "global_batch": B * world, "num_actions": A, "obs": "4x84x84 u8",
+              "parallelism": f"dp{world}", "l2": "flushed (256 MB memset) before every timed step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(T, B * world if world > 1 else B, A, args.steps, args.warmup)
+        line = {"impl": "reference", "metric": "learner env-frames/sec", "value": r["value"],
+                "unit": "env-frames/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "cpu_baseline": r,
+                "e2e": {"value": r["value"], "unit": "env-frames/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = True
+
+    from paper_1910_03552_b200 import _native as N
+    from paper_1910_03552_b200 import kernel_bench, learner, optim
+    from paper_1910_03552_b200.atari_net import AtariNet
+
+    torch.manual_seed(1234)  # identical initial weights on every rank
+    model = AtariNet(num_actions=A, device=dev)
+    opt = optim.RMSprop(model.parameters(), lr=FLAGS["learning_rate"], alpha=FLAGS["alpha"],
+                        eps=FLAGS["epsilon"])
+    batch = make_batch(T, B, A, dev, seed=100 + rank)
+    L = learner.FusedLearner(model, FLAGS, T, B, process_group=pg)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up
+    for _ in range(max(3, args.warmup)):
+        L.step(batch, opt)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident inputs
+    s = torch.cuda.current_stream()
+    launches0 = N.lib().bp_launch_count()
+    times = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            L.step(batch, opt)
+            e1.record(s)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+        barrier()
+        torch.cuda.synchronize()
+    launches = N.lib().bp_launch_count() - launches0
+    step_s = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([step_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_s = float(t)
+    value = T * B * world / step_s
+
+    # ---- e2e through the public learn() API, batch from pinned host memory
+    host = {k: v.cpu().pin_memory() for k, v in batch.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    dev_batch = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+
+    def e2e_step():
+        for k, v in host.items():
+            dev_batch[k].copy_(v, non_blocking=True)
+        return learner.learn(FLAGS, None, model, dev_batch, (), opt, None, process_group=pg)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_times = []
+    barrier()
+    for _ in range(max(3, args.steps // 2)):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        stats = e2e_step()  # ends with the D2H read of the loss stats (host sync)
+        e1.record(s)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1) * 1e-3)
+    e2e_s = statistics.mean(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t)
+
+    # ---- roofline of the dominant kernel group + the V-trace kernel (north-star ask)
+    pk = peaks()
+    br = kernel_breakdown(L, batch, opt)
+    n = (T + 1) * B
+    fwd_flops = 2 * n * sum(MACS.values())
+    bwd_flops = 2 * n * (2 * sum(MACS.values()) - MACS["conv1"])
+    dominant = max(("forward", "backward"), key=lambda k: br[k])
+    dom_flops = fwd_flops if dominant == "forward" else bwd_flops
+    achieved = dom_flops / br[dominant] / 1e12
+    roofline = {"bound": "tensor", "kernel": f"atari_{dominant} (tcgen05 GEMMs + epilogues)",
+                "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16"], "traffic": None, "peak_kind": pk["kind"],
+                "phase_seconds": br, "flops_per_launch": dom_flops}
+    timer = kernel_bench.Timer()
+    vt = kernel_bench.bench_vtrace(80, 4096, 18, timer, iters=20)
+    vt_roof = {"bound": "hbm", "kernel": "vtrace_from_logits T=80 B=4096 A=18",
+               "achieved": vt["gbs"], "peak": pk["hbm"], "unit": "GB/s",
+               "frac": vt["gbs"] / pk["hbm"], "traffic": None, "bytes": vt["bytes"],
+               "seconds": vt["median_s"]}
+    ll = kernel_bench.bench_loss(T, B, A, timer, iters=20)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(T, B, A, steps=3, warmup=1, budget_s=30.0)
+
+    if rank == 0:
+        line = {
+            "metric": "learner env-frames/sec", "value": value, "unit": "env-frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config,
+            "e2e": {"value": T * B * world / e2e_s, "unit": "env-frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 32, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
+            "roofline": roofline, "vtrace_roofline": vt_roof,
+            "learner_loss_kernel_s": ll["median_s"],
+            "cpu_baseline": cpu, "clocks": clk.summary(),
+            "stats_last": {k: stats[k] for k in ("total_loss", "pg_loss", "baseline_loss",
+                                                 "entropy_loss")},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -41,6 +41,8 @@ extern "C" {
 
 int bp_abi_version(void);
 const char* bp_last_error(void);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long bp_launch_count(void);
 
 /* ---------------------------------------------------------------------------
  * V-trace
@@ -131,6 +133,73 @@ int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t 
                         const double* sumsq, float max_norm, int clip_mode, float lr,
                         const float* lr_dev, float alpha, float eps, int write_clipped_grads,
                         float* norm_out, unsigned* status, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * AtariNet (north-star network; replaces the reference network seam
+ * mlp_forward / mlp_backward / mlp_forward_backward, model.py:126-203).
+ * All dense contractions run on tcgen05 tensor cores (bf16 operands, f32
+ * accumulate).  The caller owns every buffer; sizes are given per field for
+ * a capacity of `max_frames` frames (N = (T+1)*B rows).
+ * ------------------------------------------------------------------------- */
+typedef struct BpAtariNet {
+  int num_actions; /* A in [1, 31] */
+  int max_frames;  /* capacity N */
+  /* bf16 operand copies written by bp_atari_pack_weights */
+  void* w1f;  /* [32][256]    conv1, (Cout, K)          */
+  void* w2f;  /* [64][512]    conv2                     */
+  void* w3f;  /* [64][576]    conv3                     */
+  void* wfcf; /* [512][3136]  fc                        */
+  void* whf;  /* [32][512]    heads (A logits, baseline, zero rows) */
+  void* w2d;  /* [128][256]   conv2 data-grad operand   */
+  void* w3d;  /* [64][576]    conv3 data-grad operand   */
+  void* wfcd; /* [3136][512]  fc data-grad operand      */
+  void* whd;  /* [512][64]    heads data-grad operand   */
+  /* activations, bf16 */
+  void* x0; /* [N*441][64]  space-to-depth frames           */
+  void* x1; /* [N*100][128] conv1 out (space-to-depth 2)    */
+  void* x2; /* [N*81][64]   conv2 out                       */
+  void* x3; /* [N][3136]    conv3 out, (y, x, c) order      */
+  void* h;  /* [N][512]     relu(fc)                        */
+  /* backward temporaries, bf16.  d_pre1/2/3 MUST be zeroed once at
+   * allocation: their grid padding rows are never written. */
+  void* g;      /* [N][64]      [d_logits | d_baseline | 0]  */
+  void* d_fc;   /* [N][512]                                  */
+  void* d_pre3; /* [N*81][64]   conv3 pre-activation grad    */
+  void* d_pre2; /* [N*100][64]  conv2 pre-activation grad    */
+  void* d_pre1; /* [N*441][32]  conv1 pre-activation grad    */
+  void* ws;     /* f32 workspace, bp_atari_workspace_bytes()  */
+  size_t ws_bytes;
+} BpAtariNet;
+
+/* f32 master parameter layout (flat, upstream AtariNet module order and torch
+ * layouts): conv1.weight [32][4][8][8], conv1.bias, conv2.weight [64][32][4][4],
+ * conv2.bias, conv3.weight [64][64][3][3], conv3.bias, fc.weight [512][3136],
+ * fc.bias, policy.weight [A][513+A], policy.bias, baseline.weight [1][513+A],
+ * baseline.bias.  offsets[12] = total count. */
+int64_t bp_atari_param_count(int num_actions, int use_lstm);
+int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* offsets /* 13 */);
+size_t bp_atari_workspace_bytes(int num_actions, int max_frames);
+/* bf16 operand copies from the f32 master parameters (call after each optimiser step) */
+int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stream);
+/* Forward of n frames: frames u8 [n][4][84][84], reward [n], last_action [n] int64
+ * -> logits [n][A] f32, baseline [n] f32.  Keeps the activations for backward. */
+int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
+                     const int64_t* last_action, const float* params, float* logits,
+                     float* baseline, void* stream);
+/* Backward of the last forward: d_logits [n][A], d_baseline [n] -> grads (flat f32,
+ * same layout as params; every entry is overwritten). */
+int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
+                      const float* reward, const int64_t* last_action, float* grads, void* stream);
+/* Categorical sampling per row (Gumbel-max, counter-based hash RNG keyed by
+ * (seed, row, column)); greedy != 0 -> argmax.  Replaces sample_actions
+ * (model.py:218-221) / upstream torch.multinomial(softmax(logits)).
+ * logits [n][A] f32 -> actions [n] int64. */
+int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
+                          int64_t* actions, void* stream);
+/* Raw tcgen05 GEMM engine (test entry): C[M][N] f32 = A . B^T, bf16 operands
+ * (a_mn / b_mn select MN-major storage), split-K partials at C + s*M*N. */
+int bp_gemm_bf16_test(const void* A, const void* B, float* C, int M, int N, int K, int a_mn,
+                      int b_mn, int splits, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,4 +1,5 @@
 // C-ABI glue: version, thread-local error message, launch checking.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 
@@ -7,6 +8,7 @@
 namespace bp {
 
 static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -16,6 +18,7 @@ void set_error(const char* fmt, ...) {
 }
 
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);  // every kernel launch is followed by one check
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));
@@ -28,3 +31,4 @@ int check_launch(const char* what) {
 
 extern "C" int bp_abi_version(void) { return 1; }
 extern "C" const char* bp_last_error(void) { return bp::g_err; }
+extern "C" unsigned long long bp_launch_count(void) { return bp::g_launches.load(); }

@@ -41,6 +41,7 @@ struct GemmArgs {
   // epilogue
   int N;                 // full N (row-major ld of mask source / plain output)
   int M;                 // valid M rows (rows >= M are not stored)
+  float alpha;           // v = alpha * acc (+ bias)
   const float* bias;     // [N] or null
   int relu;              // apply max(0, .)
   const __nv_bfloat16* mask;  // relu-backward mask source, same (m, n) index, ld N; null = none
@@ -53,6 +54,17 @@ struct GemmArgs {
   // column map: C(n) = ((n/cdiv)/cq)*cs1 + ((n/cdiv)%cq)*cs2 + n%cdiv
   int cdiv, cq;
   long long cs1, cs2;
+  // AtariNet heads epilogue (heads != 0): columns j < A are policy logits, j == A
+  // the baseline; adds bias + W[:, 512] * clip(reward) + W[:, 513 + last_action]
+  int heads, A, core;          // core = 512 + 1 + A (row length of Wp / Wv)
+  const float* wp;             // [A][core]  f32 master policy weight
+  const float* bp;             // [A]
+  const float* wv;             // [core]
+  const float* bv;             // [1]
+  const float* reward;         // [M]
+  const int64_t* last_action;  // [M]
+  float* logits;               // [M][A]
+  float* baseline;             // [M]
 };
 
 template <int BN, int AM, int BM, int BSWZ>
@@ -120,9 +132,38 @@ BP_DEVICE uint32_t pack_bf16x2(float a, float b) {
 }
 
 // one row x 32 consecutive columns of the tile
+BP_DEVICE void heads_epilogue(const GemmArgs& g, int m, float (&v)[32]) {
+  const float r = fminf(fmaxf(__ldg(g.reward + m), -1.f), 1.f);
+  const int la = (int)__ldg(g.last_action + m);
+  const bool la_ok = la >= 0 && la < g.A;
+  float bsum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {  // compile-time indices keep v[] in registers
+    if (j < g.A) {
+      const float* w = g.wp + (size_t)j * g.core;
+      float x = v[j] + __ldg(g.bp + j) + __ldg(w + 512) * r;
+      if (la_ok) x += __ldg(w + 513 + la);
+      g.logits[(size_t)m * g.A + j] = x;
+    } else if (j == g.A) {
+      bsum = v[j];
+    }
+  }
+  float b = bsum + __ldg(g.bv) + __ldg(g.wv + 512) * r;
+  if (la_ok) b += __ldg(g.wv + 513 + la);
+  g.baseline[m] = b;
+}
+
 BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
                               int sp, float (&v)[32]) {
   if (!row_ok) return;
+  if (g.heads) {
+    heads_epilogue(g, m, v);
+    return;
+  }
+  if (g.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= g.alpha;
+  }
   if (g.bias) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] += __ldg(g.bias + n0 + i);

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
   float* s_ent = scan + 7 * TB;    //            entropy
   float* s_tlp = scan + 8 * TB;    //            learner log pi(a)
   int* s_act = reinterpret_cast<int*>(scan + 9 * TB);
+  int64_t* s_act64 = reinterpret_cast<int64_t*>(s_delta);  // phase-1 staging in slots 4-5
   float* s_boot = scan + plan.n_scan * TB;
 
   const int tid = threadIdx.x;
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         const int t0 = c * TC, nt = min(TC, T - t0);
         const int ntens = p3 ? 1 : 2;
         if (p3) {
-          bulk_wait_read_all();  // this stage may still be feeding d_logits bulk stores
+          bulk_wait_read_1();  // the stage's d_logits stores (all but the newest group) have read smem
           __syncwarp();
         }
         if (lane == 0) mbar_expect_tx(&full_bar[q % nst], span_bytes * nt * ntens);
@@ -290,25 +291,43 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
 
   // ----------------------------------------------------------------- phase 1
   if constexpr (MODE != MODE_IW) {
+    // Small (T, BT) inputs of the whole tile are prefetched once, up front, with
+    // cp.async straight into the smem scan arrays (thread i owns elements i + 128k,
+    // exactly the rows it processes below).  In the cp.async path they join
+    // chunk 0's commit group.
+    for (int i = tid; i < TB; i += kThreads) {
+      const int t = i / BT, b = i % BT;
+      if (b < bw) {
+        const size_t idx = (size_t)t * B + b0 + b;
+        cp_async8(s_act64 + i, g.act + idx);
+        cp_async4(s_rew + i, g.rew + idx);
+        cp_async4(s_val + i, g.val + idx);
+        if constexpr (MODE != MODE_LOSS) cp_async4(s_disc + i, g.disc + idx);
+      }
+    }
+    if constexpr (MODE == MODE_LOSS) {
+#pragma unroll 4
+      for (int i = tid; i < TB; i += kThreads) {
+        const int t = i / BT, b = i % BT;
+        if (b < bw) s_disc[i] = __ldg(g.done + (size_t)t * B + b0 + b) ? 0.f : g.discount;
+      }
+    }
+    if constexpr (BULK) cp_async_commit();
     for (int q = 0; q < nst - 1; ++q) issue(q);
     for (int c = 0; c < nchunks; ++c) {
       issue(c + nst - 1);
       const int t = c * TC + tl;
       const bool live = (t < T) && (bl < bw);
-      // small per-row inputs: plain loads issued before the wait
-      int64_t a64 = 0;
-      float rv = 0.f, vv = 0.f, dv = 0.f;
-      uint8_t dn = 0;
       const size_t idx = (size_t)t * B + b0 + bl;
-      if (live) {
-        a64 = __ldg(g.act + idx);
-        rv = __ldg(g.rew + idx);
-        vv = __ldg(g.val + idx);
-        if constexpr (MODE == MODE_LOSS) dn = __ldg(g.done + idx);
-        else dv = __ldg(g.disc + idx);
+      const int si = t * BT + bl;
+      if constexpr (BULK) {
+        if (c == 0) cp_async_wait<0>();
       }
       wait_chunk(c);
       if (live) {
+        const int64_t a64 = s_act64[si];
+        float rv = s_rew[si];
+        const float vv = s_val[si], dv = s_disc[si];
         const float* st = smem + (size_t)(c % nst) * plan.stage_floats;
         int a = (int)a64;
         if (a64 < 0 || a64 >= A) {
@@ -321,18 +340,17 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         const float tlp = rt.xa - rt.lse;
         const float lr = tlp - blp;
         if constexpr (MODE == MODE_LOSS) {
-          dv = dn ? 0.f : g.discount;  // (float)gamma * ~done, exact
-          if (g.reward_clip) rv = fminf(fmaxf(rv, -1.f), 1.f);
+          // discount = (float)gamma * ~done, exact (set in the prefetch above)
+          if (g.reward_clip) {
+            rv = fminf(fmaxf(rv, -1.f), 1.f);
+            s_rew[si] = rv;
+          }
         } else {
           if (dv < 0.f) bad |= BP_STATUS_NEG_DISCOUNT;
         }
         if (!(rb.finite && rt.finite && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(dv)))
           bad |= BP_STATUS_NONFINITE_IN;
-        const int si = t * BT + bl;
         s_lr[si] = lr;
-        s_disc[si] = dv;
-        s_rew[si] = rv;
-        s_val[si] = vv;
         if constexpr (MODE == MODE_LOSS) {
           s_lse[si] = rt.lse;
           s_ent[si] = rt.ent;
@@ -470,7 +488,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
     // ------------------------------------------------------- phase 3b: d_logits
     for (int c = 0; c < nchunks; ++c) {
       const int q = nchunks + c;
-      issue(q + nst - 1);
+      if constexpr (!BULK) issue(q + nst - 1);
       wait_chunk(q);
       float* st = smem + (size_t)(q % nst) * plan.stage_floats;
       const int t0 = c * TC, nt = min(TC, T - t0);
@@ -488,6 +506,8 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
             bulk_s2g(g.d_logits + ((size_t)(t0 + r) * B + b0) * A, st + r * RS, span_bytes);
           bulk_commit();
         }
+        // refill the stage whose stores were issued one iteration ago
+        issue(q + nst - 1);
       } else {
         __syncthreads();
         const int span = bw * A;

@@ -1,0 +1,135 @@
+"""The IMPALA learner step: upstream TorchBeast `learn()` as a fused device pipeline.
+
+Replaces LearnerContext.train_batch (pipeline.py:297-373) +
+SharedModel.apply_gradients (pipeline.py:247-251) -- and upstream
+`monobeast.learn(flags, actor_model, model, batch, initial_agent_state,
+optimizer, scheduler, lock)` [upstream, not vendored] with the same signature.
+
+One step = (all on the current CUDA stream, no host sync until stats are read)
+  1. AtariNet forward on (T+1)*B frames          bp_atari_forward   (tcgen05)
+  2. fused V-trace + 3 losses + d_logits/d_base  bp_learner_loss_f32
+  3. AtariNet backward -> flat f32 gradients     bp_atari_backward  (tcgen05)
+  4. [DP] NCCL all-reduce(SUM) of the flat gradient buffer (torch.distributed)
+  5. global-norm clip + RMSProp                  bp_sumsq_f32 + bp_rmsprop_clip_f32
+
+Row alignment follows upstream (`batch[1:]` for actions / behaviour logits /
+rewards / done, learner outputs rows [:-1], bootstrap = baseline[-1]).
+"""
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _native as N  # noqa: F401  (fail loudly if the library is missing)
+from .errors import SchemaError
+from .learner_ops import LearnerLoss, VtraceConfig
+from .optim import RMSprop, sumsq_
+
+
+def _flag(flags, name, default=None):
+    if isinstance(flags, dict):
+        return flags.get(name, default)
+    return getattr(flags, name, default)
+
+
+class FusedLearner:
+    """Preallocated learner step for one (model, T, B); `step()` enqueues only."""
+
+    def __init__(self, model, flags, unroll_length: int, batch_size: int, process_group=None):
+        self.model = model
+        self.T = unroll_length
+        self.B = batch_size
+        self.n = (unroll_length + 1) * batch_size
+        dev = model.flat_params.device
+        A = model.num_actions
+        self.cfg = VtraceConfig(
+            discount=float(_flag(flags, "discounting", 0.99)),
+            baseline_cost=float(_flag(flags, "baseline_cost", 0.5)),
+            entropy_cost=float(_flag(flags, "entropy_cost", 0.0006)),
+            reward_clip=_flag(flags, "reward_clipping", "abs_one") == "abs_one",
+            row_shift=1)
+        self.max_norm = float(_flag(flags, "grad_norm_clipping", 40.0))
+        self.loss = LearnerLoss(dev)
+        self.logits = torch.empty(self.n, A, device=dev)
+        self.baseline = torch.empty(self.n, device=dev)
+        self.d_logits = torch.zeros(self.n, A, device=dev)  # row T stays zero
+        self.d_baseline = torch.zeros(self.n, device=dev)
+        self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.pg = process_group
+        model.buffers_for(self.n)
+
+    def step(self, batch, optimizer=None, scheduler=None):
+        """Enqueue one learner step on the current stream; returns the device loss vector."""
+        m, T, B, n = self.model, self.T, self.B, self.n
+        frames = batch["frame"]
+        if tuple(frames.shape[:2]) != (T + 1, B):
+            raise SchemaError(f"frame dims {tuple(frames.shape)}, expected ({T + 1}, {B}, ...)")
+        A = m.num_actions
+        reward = batch["reward"]
+        last_action = batch["last_action"]
+        # 1. forward
+        m._forward_kernels(frames.reshape(n, *m.observation_shape), reward.reshape(n),
+                           last_action.reshape(n), logits=self.logits, baseline=self.baseline)
+        # 2. fused V-trace + losses + gradients w.r.t. logits / baseline
+        self.loss(self.logits[:T * B].view(T, B, A), self.baseline.view(T + 1, B),
+                  batch["policy_logits"][1:], batch["action"][1:], reward[1:], batch["done"][1:],
+                  self.cfg, d_logits=self.d_logits[:T * B].view(T, B, A),
+                  d_baseline=self.d_baseline.view(T + 1, B), losses=self.losses)
+        # 3. backward into the flat gradient buffer
+        m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
+                            m.flat_grads)
+        # 4. data-parallel: sum gradients over ranks (losses are sums over T x B)
+        if self.pg is not None:
+            torch.distributed.all_reduce(m.flat_grads, op=torch.distributed.ReduceOp.SUM,
+                                         group=self.pg if self.pg is not True else None)
+        # 5. clip + RMSProp
+        if optimizer is not None:
+            if isinstance(optimizer, RMSprop) and optimizer.flat_params.data_ptr() == m.flat_params.data_ptr():
+                optimizer.step(max_norm=self.max_norm)
+            else:  # any torch optimiser: device-side norm + clip, then its own step
+                ss = torch.zeros(1, dtype=torch.float64, device=m.flat_grads.device)
+                sumsq_(m.flat_grads, ss)
+                coef = torch.clamp(self.max_norm / (ss.sqrt().float() + 1e-6), max=1.0)
+                m.flat_grads.mul_(coef)
+                optimizer.step()
+        if scheduler is not None:
+            scheduler.step()
+        return self.losses
+
+    def stats(self, batch, losses=None):
+        """Upstream learn() stats dict (reads the loss vector back: one sync)."""
+        lv = (self.losses if losses is None else losses).tolist()
+        pg, base, ent, total = lv
+        cfg = self.cfg
+        done = batch["done"][1:]
+        ep = batch.get("episode_return") if isinstance(batch, dict) else None
+        returns = ep[1:][done] if ep is not None else torch.zeros(0)
+        returns = returns.float().cpu()
+        return {
+            "episode_returns": tuple(returns.numpy()),
+            "mean_episode_return": float(returns.mean()) if returns.numel() else float("nan"),
+            "total_loss": total,
+            "pg_loss": pg * cfg.pg_cost,
+            "baseline_loss": base * cfg.baseline_cost,
+            "entropy_loss": ent * cfg.entropy_cost,
+        }
+
+
+def learn(flags, actor_model, model, batch, initial_agent_state, optimizer, scheduler,
+          lock=threading.Lock(), process_group=None):
+    """Upstream `learn()` signature; performs the fused step and returns the stats dict."""
+    with lock:
+        T1, B = batch["frame"].shape[:2]
+        key = (T1 - 1, B)
+        fl = getattr(model, "_fused_learners", None)
+        if fl is None:
+            fl = model._fused_learners = {}
+        L = fl.get(key)
+        if L is None:
+            L = fl[key] = FusedLearner(model, flags, T1 - 1, B, process_group)
+        L.step(batch, optimizer, scheduler)
+        stats = L.stats(batch)
+        if actor_model is not None and actor_model is not model:
+            actor_model.load_state_dict(model.state_dict())
+        return stats

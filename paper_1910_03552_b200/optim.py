@@ -85,6 +85,20 @@ def _is_flat(params, flat) -> bool:
     return off == flat.numel()
 
 
+def _flat_view(tensors):
+    """If `tensors` are contiguous, in-order views of one f32 storage, return a flat view of them."""
+    if not tensors or any(t is None or t.dtype != torch.float32 or not t.is_contiguous() for t in tensors):
+        return None
+    st = tensors[0].untyped_storage()
+    off0 = tensors[0].storage_offset()
+    off = off0
+    for t in tensors:
+        if t.untyped_storage().data_ptr() != st.data_ptr() or t.storage_offset() != off:
+            return None
+        off += t.numel()
+    return tensors[0].detach().new_empty(0).set_(st, off0, (off - off0,))
+
+
 class RMSprop(torch.optim.Optimizer):
     """torch.optim.RMSprop-compatible optimiser with a fused clip + update kernel.
 
@@ -101,8 +115,12 @@ class RMSprop(torch.optim.Optimizer):
         super().__init__(params, defaults)
         plist = [p for g in self.param_groups for p in g["params"]]
         self.device = plist[0].device
+        fp = _flat_view([p.data for p in plist])
+        fg = _flat_view([p.grad for p in plist]) if fp is not None else None
         if flat is not None and _is_flat(plist, flat[0]):
             self.flat_params, self.flat_grads = flat
+        elif fp is not None and fg is not None:  # e.g. AtariNet: params already flat
+            self.flat_params, self.flat_grads = fp, fg
         else:
             self.flat_params, self.flat_grads = flatten_params_(plist, self.device)
         self.square_avg = torch.zeros_like(self.flat_params)
