@@ -128,11 +128,13 @@ int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* workspace, void
  * square_avg and params are updated in place; grads are overwritten with the
  * clipped gradients when write_clipped_grads != 0 (torch semantics).
  * norm_out (nullable, device f32) receives the pre-clip norm.  lr is read
- * from *lr_dev when non-null (device-side LR schedule), else `lr`. */
+ * from *lr_dev when non-null (device-side LR schedule), else `lr`.
+ * bf16_mirror (nullable, n bf16) receives the updated parameters in bf16 (the
+ * GEMM operand copy of BpAtariNet.wbf), fused into the same pass. */
 int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t n,
                         const double* sumsq, float max_norm, int clip_mode, float lr,
                         const float* lr_dev, float alpha, float eps, int write_clipped_grads,
-                        float* norm_out, unsigned* status, void* stream);
+                        float* norm_out, void* bf16_mirror, unsigned* status, void* stream);
 
 /* ---------------------------------------------------------------------------
  * AtariNet (north-star network; replaces the reference network seam
@@ -144,22 +146,19 @@ int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t 
 typedef struct BpAtariNet {
   int num_actions; /* A in [1, 31] */
   int max_frames;  /* capacity N */
-  /* bf16 operand copies written by bp_atari_pack_weights */
-  void* w1f;  /* [32][256]    conv1, (Cout, K)          */
-  void* w2f;  /* [64][512]    conv2                     */
-  void* w3f;  /* [64][576]    conv3                     */
-  void* wfcf; /* [512][3136]  fc                        */
-  void* whf;  /* [32][512]    heads (A logits, baseline, zero rows) */
-  void* w2d;  /* [128][256]   conv2 data-grad operand   */
-  void* w3d;  /* [64][576]    conv3 data-grad operand   */
-  void* wfcd; /* [3136][512]  fc data-grad operand      */
-  void* whd;  /* [512][64]    heads data-grad operand   */
+  void* wbf;  /* bf16 mirror of the flat f32 parameters (GEMM operands) */
+  void* whf;  /* [32][576] bf16 heads operand: [Wp | bp], [Wv | bv], zero rows */
   /* activations, bf16 */
-  void* x0; /* [N*441][64]  space-to-depth frames           */
-  void* x1; /* [N*100][128] conv1 out (space-to-depth 2)    */
-  void* x2; /* [N*81][64]   conv2 out                       */
-  void* x3; /* [N][3136]    conv3 out, (y, x, c) order      */
-  void* h;  /* [N][512]     relu(fc)                        */
+  void* x0;   /* [N*441][64]  space-to-depth frames           */
+  void* x1;   /* [N*100][128] conv1 out (space-to-depth 2)    */
+  void* x2;   /* [N*81][64]   conv2 out                       */
+  void* x3;   /* [N][3136]    conv3 out, (y, x, c) order      */
+  void* core; /* [N][576]     [relu(fc) | clip(r) | onehot(a) | 1 | 0]  */
+  /* relu masks (1 bit per activation element, same layout), u32 words */
+  void* m1;   /* [N*100*4]  of x1 */
+  void* m2;   /* [N*81*2]   of x2 */
+  void* m3;   /* [N*98]     of x3 */
+  void* mc;   /* [N*18]     of core */
   /* backward temporaries, bf16.  d_pre1/2/3 MUST be zeroed once at
    * allocation: their grid padding rows are never written. */
   void* g;      /* [N][64]      [d_logits | d_baseline | 0]  */
@@ -171,15 +170,20 @@ typedef struct BpAtariNet {
   size_t ws_bytes;
 } BpAtariNet;
 
-/* f32 master parameter layout (flat, upstream AtariNet module order and torch
- * layouts): conv1.weight [32][4][8][8], conv1.bias, conv2.weight [64][32][4][4],
- * conv2.bias, conv3.weight [64][64][3][3], conv3.bias, fc.weight [512][3136],
- * fc.bias, policy.weight [A][513+A], policy.bias, baseline.weight [1][513+A],
- * baseline.bias.  offsets[12] = total count. */
+/* f32 master parameter layout (flat, upstream AtariNet module order):
+ * conv1.weight, conv1.bias, conv2.weight, conv2.bias, conv3.weight, conv3.bias,
+ * fc.weight, fc.bias, policy.weight [A][513+A], policy.bias,
+ * baseline.weight [1][513+A], baseline.bias; offsets[12] = total count.
+ * Conv / fc weights are stored in GEMM layout [Cout][K], K = (tap, channel):
+ *   conv1 k = (dy*2+dx)*64 + ci*16 + ry*4 + rx   (ky = 4dy+ry, kx = 4dx+rx)
+ *   conv2 k = (dy*2+dx)*128 + (py*2+px)*32 + c    (ky = 2dy+py, kx = 2dx+px)
+ *   conv3 k = (dy*3+dx)*64 + c;   fc k = (y*7+x)*64 + c
+ * (the Python module converts to / from the torch layouts in state_dicts). */
 int64_t bp_atari_param_count(int num_actions, int use_lstm);
 int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* offsets /* 13 */);
 size_t bp_atari_workspace_bytes(int num_actions, int max_frames);
-/* bf16 operand copies from the f32 master parameters (call after each optimiser step) */
+/* bf16 mirror of the f32 master parameters (needed after parameters change outside
+ * bp_rmsprop_clip_f32 with a mirror output, e.g. after load / init) */
 int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stream);
 /* Forward of n frames: frames u8 [n][4][84][84], reward [n], last_action [n] int64
  * -> logits [n][A] f32, baseline [n] f32.  Keeps the activations for backward. */
@@ -196,10 +200,11 @@ int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const
  * logits [n][A] f32 -> actions [n] int64. */
 int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
                           int64_t* actions, void* stream);
-/* Raw tcgen05 GEMM engine (test entry): C[M][N] f32 = A . B^T, bf16 operands
- * (a_mn / b_mn select MN-major storage), split-K partials at C + s*M*N. */
-int bp_gemm_bf16_test(const void* A, const void* B, float* C, int M, int N, int K, int a_mn,
-                      int b_mn, int splits, void* stream);
+/* Raw tcgen05 GEMM engine (test entry): C[M][N] = A . B^T, bf16 operands
+ * (a_mn / b_mn select MN-major storage), f32 output (bf16 if out_bf16), split-K
+ * partials at C + s*M*N. */
+int bp_gemm_bf16_test(const void* A, const void* B, void* C, int M, int N, int K, int a_mn,
+                      int b_mn, int splits, int out_bf16, void* stream);
 
 #ifdef __cplusplus
 }

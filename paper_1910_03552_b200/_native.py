@@ -35,7 +35,7 @@ SIGNATURES: dict[str, tuple] = {
                                 P, P, P, P, P, P, P, P]),
     "bp_sumsq_workspace_bytes": (SZ, [I64]),
     "bp_sumsq_f32": (I, [P, I64, P, P, P]),
-    "bp_rmsprop_clip_f32": (I, [P, P, P, I64, P, F, I, F, P, F, F, I, P, P, P]),
+    "bp_rmsprop_clip_f32": (I, [P, P, P, I64, P, F, I, F, P, F, F, I, P, P, P, P]),
     "bp_atari_param_count": (I64, [I, I]),
     "bp_atari_param_offsets": (I, [I, I, P]),
     "bp_atari_workspace_bytes": (SZ, [I, I]),
@@ -43,7 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_forward": (I, [P, I, P, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
-    "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, P]),
+    "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),
 }
 
 
@@ -52,8 +52,8 @@ class BpAtariNet(C.Structure):
 
     _fields_ = [("num_actions", C.c_int), ("max_frames", C.c_int)] + [
         (name, C.c_void_p) for name in (
-            "w1f", "w2f", "w3f", "wfcf", "whf", "w2d", "w3d", "wfcd", "whd",
-            "x0", "x1", "x2", "x3", "h", "g", "d_fc", "d_pre3", "d_pre2", "d_pre1", "ws")
+            "wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
+            "d_pre3", "d_pre2", "d_pre1", "ws")
     ] + [("ws_bytes", C.c_size_t)]
 
 

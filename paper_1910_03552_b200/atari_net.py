@@ -1,7 +1,7 @@
 """AtariNet (upstream TorchBeast monobeast.AtariNet) on the sm_100a kernels.
 
 Drop-in for `AtariNet(observation_shape, num_actions, use_lstm=False)`:
-same submodule names / parameter shapes / state_dict keys as upstream
+same submodule names and state_dict keys / shapes / layouts as upstream
 (conv1, conv2, conv3, fc, policy, baseline), same `forward(inputs,
 core_state) -> (dict(policy_logits, baseline, action), core_state)` and
 `initial_state(batch_size)`.  The reference network seam it replaces is
@@ -11,7 +11,9 @@ Every dense contraction runs on tcgen05 tensor cores through the C ABI
 (bp_atari_forward / bp_atari_backward; bf16 operands, f32 accumulation).
 Parameters are views into one flat f32 buffer (`flat_params`), gradients
 into `flat_grads`, so the fused optimiser and the NCCL all-reduce see one
-contiguous buffer each.
+contiguous buffer each.  The conv / fc weight Parameters hold the kernels'
+[Cout][K] GEMM layout (`torch_to_gemm`); `state_dict()` / `load_state_dict()`
+convert to / from the upstream torch layouts, so checkpoints interoperate.
 
 Autograd: `forward` is an autograd.Function whose backward calls the fused
 backward kernels, so `total_loss.backward()` works as upstream.  `learn()`
@@ -30,10 +32,39 @@ from .errors import DimensionError
 OBS_SHAPE = (4, 84, 84)
 
 
+def torch_to_gemm(name: str, w: torch.Tensor) -> torch.Tensor:
+    """Upstream torch weight layout -> the [Cout][K] GEMM layout of the kernels
+    (K = (tap, input channel), include/beast_b200.h)."""
+    if name == "conv1.weight":  # [32][4][8][8], ky = 4dy+ry, kx = 4dx+rx
+        return w.reshape(32, 4, 2, 4, 2, 4).permute(0, 2, 4, 1, 3, 5).reshape(32, 256)
+    if name == "conv2.weight":  # [64][32][4][4], ky = 2dy+py, kx = 2dx+px
+        return w.reshape(64, 32, 2, 2, 2, 2).permute(0, 2, 4, 3, 5, 1).reshape(64, 512)
+    if name == "conv3.weight":  # [64][64][3][3]
+        return w.permute(0, 2, 3, 1).reshape(64, 576)
+    if name == "fc.weight":  # [512][3136], torch feature c*49 + pos -> k = pos*64 + c
+        return w.reshape(512, 64, 49).permute(0, 2, 1).reshape(512, 3136)
+    return w
+
+
+def gemm_to_torch(name: str, w: torch.Tensor) -> torch.Tensor:
+    if name == "conv1.weight":
+        return w.reshape(32, 2, 2, 4, 4, 4).permute(0, 3, 1, 4, 2, 5).reshape(32, 4, 8, 8)
+    if name == "conv2.weight":
+        return w.reshape(64, 2, 2, 2, 2, 32).permute(0, 5, 1, 3, 2, 4).reshape(64, 32, 4, 4)
+    if name == "conv3.weight":
+        return w.reshape(64, 3, 3, 64).permute(0, 3, 1, 2)
+    if name == "fc.weight":
+        return w.reshape(512, 49, 64).permute(0, 2, 1).reshape(512, 3136)
+    return w
+
+
+GEMM_WEIGHTS = ("conv1.weight", "conv2.weight", "conv3.weight", "fc.weight")
+
+
 class _Buffers:
     """Caller-owned device buffers of the C ABI struct BpAtariNet, for n <= capacity."""
 
-    def __init__(self, num_actions: int, capacity: int, device):
+    def __init__(self, num_actions: int, capacity: int, nparams: int, device):
         self.capacity = capacity
         d = device
         bf = torch.bfloat16
@@ -46,18 +77,20 @@ class _Buffers:
 
         n = capacity
         self.t = dict(
-            w1f=e(32, 256), w2f=e(64, 512), w3f=e(64, 576), wfcf=e(512, 3136), whf=e(32, 512),
-            w2d=e(128, 256), w3d=e(64, 576), wfcd=e(3136, 512), whd=e(512, 64),
-            x0=e(n * 441, 64), x1=e(n * 100, 128), x2=e(n * 81, 64), x3=e(n, 3136), h=e(n, 512),
+            wbf=e(nparams), whf=e(32, 576),
+            x0=e(n * 441, 64), x1=e(n * 100, 128), x2=e(n * 81, 64), x3=e(n, 3136), core=e(n, 576),
+            m1=e(n * 400, dtype=torch.int32), m2=e(n * 162, dtype=torch.int32),
+            m3=e(n * 98, dtype=torch.int32), mc=e(n * 18, dtype=torch.int32),
             g=e(n, 64), d_fc=e(n, 512),
             # grid padding rows of these are never written: zero once
             d_pre3=z(n * 81, 64), d_pre2=z(n * 100, 64), d_pre1=z(n * 441, 32),
         )
         ws_bytes = N.lib().bp_atari_workspace_bytes(num_actions, capacity)
         self.t["ws"] = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=d)
-        self.struct = N.BpAtariNet(num_actions, capacity, *[self.t[k].data_ptr() for k in (
-            "w1f", "w2f", "w3f", "wfcf", "whf", "w2d", "w3d", "wfcd", "whd", "x0", "x1", "x2",
-            "x3", "h", "g", "d_fc", "d_pre3", "d_pre2", "d_pre1", "ws")], ws_bytes)
+        names = ("wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
+                 "d_pre3", "d_pre2", "d_pre1", "ws")
+        self.struct = N.BpAtariNet(num_actions, capacity, *[self.t[k].data_ptr() for k in names],
+                                   ws_bytes)
         self.ref = C.byref(self.struct)
 
 
@@ -101,6 +134,12 @@ class AtariNet(nn.Module):
         self.policy = nn.Linear(core, num_actions)
         self.baseline = nn.Linear(core, 1)
         self.to(device)
+        # conv / fc weights live in the kernels' [Cout][K] GEMM layout; state_dict() and
+        # load_state_dict() convert to / from the upstream torch layouts (hooks below)
+        with torch.no_grad():
+            for name in GEMM_WEIGHTS:
+                mod = getattr(self, name.split(".")[0])
+                mod.weight = nn.Parameter(torch_to_gemm(name, mod.weight.detach()).contiguous())
         count = N.lib().bp_atari_param_count(num_actions, 0)
         params = list(self.parameters())
         assert sum(p.numel() for p in params) == count
@@ -115,35 +154,72 @@ class AtariNet(nn.Module):
             p.grad = self.flat_grads[off:off + n].view_as(p)
             self._shapes.append((off, n, p.shape))
             off += n
+        self._register_state_dict_hook(AtariNet._to_torch_layout)
+        self.register_load_state_dict_pre_hook(AtariNet._from_torch_layout)
         self._bufs: _Buffers | None = None
         self._logits = None
         self._baseline = None
         self.sample_seed = 0x5EED
         self._calls = 0
+        self.mirror_fresh = False  # bf16 operand mirror (wbf) up to date with flat_params
+
+    @staticmethod
+    def _to_torch_layout(module, state_dict, prefix, local_metadata):
+        for name in GEMM_WEIGHTS:
+            k = prefix + name
+            if k in state_dict:
+                state_dict[k] = gemm_to_torch(name, state_dict[k]).contiguous()
+        return state_dict
+
+    @staticmethod
+    def _from_torch_layout(module, state_dict, prefix, local_metadata, strict, missing_keys,
+                           unexpected_keys, error_msgs):
+        # state_dicts are always in the upstream torch layout (state_dict() emits it too)
+        for name in GEMM_WEIGHTS:
+            k = prefix + name
+            if k in state_dict:
+                state_dict[k] = torch_to_gemm(name, state_dict[k]).contiguous()
+        module.mirror_fresh = False
 
     # ------------------------------------------------------------------ helpers
     def _split(self, flat):
         return [flat[o:o + n].view(s) for o, n, s in self._shapes]
 
+    def torch_layout_grads(self, flat):
+        """{name: gradient in the upstream torch layout} of a flat gradient buffer."""
+        names = [k for k, _ in self.named_parameters()]
+        return {k: gemm_to_torch(k, v) for k, v in zip(names, self._split(flat))}
+
     def buffers_for(self, n: int) -> _Buffers:
         if self._bufs is None or self._bufs.capacity < n:
-            self._bufs = _Buffers(self.num_actions, n, self.flat_params.device)
+            self._bufs = _Buffers(self.num_actions, n, self.flat_params.numel(), self.flat_params.device)
             self._logits = torch.empty(n, self.num_actions, device=self.flat_params.device)
             self._baseline = torch.empty(n, device=self.flat_params.device)
+            self.mirror_fresh = False
         return self._bufs
 
+    @property
+    def flat_bf16(self) -> torch.Tensor:
+        """bf16 mirror of flat_params: the GEMM operand the kernels read."""
+        return self.buffers_for(1).t["wbf"]
+
     def pack_weights(self) -> None:
-        """bf16 GEMM operand copies of the current f32 parameters (one kernel)."""
+        """Refresh the bf16 operand mirror from the f32 parameters (one cast kernel)."""
         b = self.buffers_for(1)
         N.check(N.lib().bp_atari_pack_weights(b.ref, N.ptr(self.flat_params),
                                               N.stream_handle(self.flat_params.device)),
                 "bp_atari_pack_weights")
+        self.mirror_fresh = True
 
-    def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None):
-        """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline."""
+    def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
+                         repack: bool = True):
+        """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
+
+        repack=False trusts the bf16 mirror (kept fresh by the fused optimiser step)."""
         n = frames.shape[0]
         b = self.buffers_for(n)
-        self.pack_weights()
+        if repack or not self.mirror_fresh:
+            self.pack_weights()
         if logits is None:
             logits = torch.empty(n, self.num_actions, device=frames.device)
         if baseline is None:

@@ -19,9 +19,13 @@
 // gradient grids; weight gradients reduce over grid rows with MN-major operands
 // and split-K partials reduced deterministically.
 //
-// Master parameters (f32, flat, see bp_atari_param_offsets) keep the upstream
-// torch layouts (state_dict compatible); bp_atari_pack_weights gathers them into
-// the bf16 GEMM operand copies and the weight-gradient finalize scatters back.
+// Master parameters (f32, flat, see bp_atari_param_offsets) keep the conv / fc
+// weights in GEMM layout [Cout][K] (K = (tap, input channel)); the Python module
+// converts state_dicts to / from the upstream torch layouts.  A bf16 mirror of
+// the flat buffer (written by the optimiser kernel, or bp_atari_pack_weights)
+// is the GEMM operand for the forward (K-major B) and the data-gradients
+// (MN-major B, same buffer); the policy / baseline heads are one GEMM over the
+// augmented core [relu(fc) | clip(r) | onehot(a) | 1].
 #include <cudaTypedefs.h>
 
 #include <cstring>
@@ -104,6 +108,7 @@ static GemmArgs base_args() {
   g.gh = g.gw = g.vh = g.vw = g.sy = g.sx = 1;
   g.cdiv = 1 << 30;
   g.cq = 1;
+  g.b_kb_per_tap = 1 << 30;
   return g;
 }
 
@@ -126,19 +131,30 @@ static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorM
   return check_launch("umma_gemm_kernel");
 }
 
-static int splits_for(int tiles_mn, int num_kb) {
-  int sp = (g_num_sms + tiles_mn - 1) / tiles_mn;
-  if (sp > num_kb) sp = num_kb;
-  return sp < 1 ? 1 : sp;
-}
+
 
 // ============================================================ support kernels
 
-// u8 frames [N,4,84,84] -> X0 [N*21*21, 64] bf16, channel = ci*16 + ry*4 + rx
+constexpr int kCoreW = 576;  // augmented core row: 512 fc + clip(r) + onehot(A) + 1 + zero pad
+
+// u8 frames [N,4,84,84] -> X0 [N*21*21, 64] bf16, channel = ci*16 + ry*4 + rx.
+// The Y == 0 CTA of each image also writes the augmented core columns 512..575:
+// [clip(reward), onehot(last_action) (A), 1 (bias), 0 ...]  (core order of upstream AtariNet).
 __global__ void __launch_bounds__(128) frames_s2d_kernel(const uint8_t* __restrict__ frames,
-                                                         __nv_bfloat16* __restrict__ x0) {
+                                                         __nv_bfloat16* __restrict__ x0,
+                                                         const float* __restrict__ reward,
+                                                         const int64_t* __restrict__ last_action,
+                                                         __nv_bfloat16* __restrict__ core, int A) {
   __shared__ __align__(16) uint8_t slab[4][4][84];
   const int img = blockIdx.x / 21, Y = blockIdx.x % 21;
+  if (Y == 0 && threadIdx.x < 64) {
+    const int j = threadIdx.x;
+    float v = 0.f;
+    if (j == 0) v = fminf(fmaxf(reward[img], -1.f), 1.f);
+    else if (j <= A) v = (last_action[img] == j - 1) ? 1.f : 0.f;
+    else if (j == A + 1) v = 1.f;
+    core[(size_t)img * kCoreW + 512 + j] = __float2bfloat16_rn(v);
+  }
   for (int w = threadIdx.x; w < 16 * 21; w += 128) {
     const int row = w / 21, col = w % 21;  // row = ci*4 + ry
     const int ci = row >> 2, ry = row & 3;
@@ -180,134 +196,30 @@ __global__ void pack_g_kernel(const float* __restrict__ dlog, const float* __res
                  pack_bf16x2(v[6], v[7]));
 }
 
-// ---- torch-layout <-> shifted-GEMM K index.  Master parameters keep the
-// upstream torch layouts (conv: [Cout][Cin][kh][kw], fc: [512][3136] with
-// features in (c, y, x) order); the GEMMs use K = (tap, input channel).
-//   L=1 conv1: k = (dy*2+dx)*64 + ci*16 + ry*4 + rx,  ky = 4dy+ry, kx = 4dx+rx
-//   L=2 conv2: k = (dy*2+dx)*128 + (py*2+px)*32 + c,  ky = 2dy+py, kx = 2dx+px
-//   L=3 conv3: k = (dy*3+dx)*64 + c
-//   L=4 fc   : k = (y*7+x)*64 + c  -> torch feature c*49 + y*7 + x
-BP_DEVICE long long torch_w_index(int L, int co, int k) {
-  if (L == 1) {
-    const int tap = k >> 6, c = k & 63, dy = tap >> 1, dx = tap & 1;
-    const int ci = c >> 4, ry = (c >> 2) & 3, rx = c & 3;
-    return (((long long)co * 4 + ci) * 8 + 4 * dy + ry) * 8 + 4 * dx + rx;
-  } else if (L == 2) {
-    const int tap = k >> 7, cc = k & 127, dy = tap >> 1, dx = tap & 1;
-    const int q = cc >> 5, c = cc & 31, py = q >> 1, px = q & 1;
-    return (((long long)co * 32 + c) * 4 + 2 * dy + py) * 4 + 2 * dx + px;
-  } else if (L == 3) {
-    const int tap = k >> 6, c = k & 63, dy = tap / 3, dx = tap % 3;
-    return (((long long)co * 64 + c) * 3 + dy) * 3 + dx;
-  } else {
-    const int pos = k >> 6, c = k & 63;
-    return (long long)co * 3136 + c * 49 + pos;
-  }
-}
-
-struct PackJob {
-  const float* src;   // torch-layout weight
-  __nv_bfloat16* dst;
-  int kind;           // 0 fwd [Cout][K]; 1 conv dgrad [Cin][taps*Cout]; 2 fc dgrad [3136][512];
-                      // 3 heads fwd Whf[32][512]; 4 heads dgrad Whd[512][64]
-  int L, cout, K, cin, taps;
-};
-struct PackArgs {
-  PackJob job[10];
-  int njobs;
-  const float* wp;
-  const float* wv;
-  int A, core;
-};
-
-__global__ void pack_weights_kernel(const __grid_constant__ PackArgs a) {
-  const PackJob& j = a.job[blockIdx.y];
-  const long long total = j.kind == 3 ? 32 * 512 : j.kind == 4 ? 512 * 64 : (long long)j.cout * j.K;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+// flat f32 -> bf16 mirror (all parameters), vectorised
+__global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, long long n) {
+  const long long n4 = n >> 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
-    float v;
-    if (j.kind == 0) {
-      const int co = (int)(i / j.K), k = (int)(i % j.K);
-      v = j.src[torch_w_index(j.L, co, k)];
-    } else if (j.kind == 1) {
-      const int row = j.taps * j.cout;
-      const int cin = (int)(i / row), r = (int)(i % row);
-      const int tap = r / j.cout, co = r % j.cout;
-      v = j.src[torch_w_index(j.L, co, tap * j.cin + cin)];
-    } else if (j.kind == 2) {
-      const int f = (int)(i / 512), o = (int)(i % 512);
-      v = j.src[torch_w_index(4, o, f)];
-    } else if (j.kind == 3) {  // Whf[aa][k], aa < 32, k < 512
-      const int aa = (int)(i / 512), k = (int)(i % 512);
-      v = aa < a.A ? a.wp[(size_t)aa * a.core + k] : (aa == a.A ? a.wv[k] : 0.f);
-    } else {  // Whd[k][aa], k < 512, aa < 64
-      const int k = (int)(i / 64), aa = (int)(i % 64);
-      v = aa < a.A ? a.wp[(size_t)aa * a.core + k] : (aa == a.A ? a.wv[k] : 0.f);
-    }
-    j.dst[i] = __float2bfloat16_rn(v);
+    const float4 v = reinterpret_cast<const float4*>(src)[i];
+    reinterpret_cast<uint2*>(dst)[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
   }
+  for (long long i = (n4 << 2) + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
 }
 
-// ---- column sums (bias gradients): src bf16 [rows][C] -> partial[cta][C]
-struct ColsumJob {
-  const __nv_bfloat16* src;
-  long long rows;
-  int C;
-  float* partial;  // [ctas][C]
-};
-struct ColsumArgs {
-  ColsumJob job[4];
-  int ctas;  // per job
-};
-
-__global__ void __launch_bounds__(256) colsum_kernel(const __grid_constant__ ColsumArgs a) {
-  const ColsumJob& j = a.job[blockIdx.y];
-  const int groups = j.C / 8;          // 8 columns per thread
-  const int rlanes = 256 / groups;     // rows in flight
-  const int cg = threadIdx.x % groups, rl = threadIdx.x / groups;
-  const long long per = (j.rows + a.ctas - 1) / a.ctas;
-  const long long r0 = (long long)blockIdx.x * per, r1 = min(j.rows, r0 + per);
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (rl < rlanes) {
-    for (long long r = r0 + rl; r < r1; r += rlanes) {
-      const uint4 w = __ldcs(reinterpret_cast<const uint4*>(j.src + r * j.C + cg * 8));
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&w);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += __bfloat162float(h[k]);
-    }
-  }
-  __shared__ float red[256][9];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) red[threadIdx.x][k] = acc[k];
-  __syncthreads();
-  for (int c = threadIdx.x; c < j.C; c += 256) {
-    const int g = c / 8, k = c % 8;
-    float s = 0.f;
-    for (int l = 0; l < rlanes; ++l) s += red[l * groups + g][k];
-    j.partial[(size_t)blockIdx.x * j.C + c] = s;
-  }
-}
-
-// ---- heads auxiliary gradients: bias, reward column, one-hot columns.
-// out partial[cta][(A+1)*(A+2)]: for a in [0, A]: [bias, reward, onehot_0..onehot_{A-1}]
-__global__ void __launch_bounds__(512) heads_aux_kernel(const float* __restrict__ dlog,
-                                                        const float* __restrict__ dbase,
-                                                        const float* __restrict__ reward,
-                                                        const int64_t* __restrict__ last_action,
-                                                        int n, int A, float* __restrict__ partial) {
-  const int nout = (A + 1) * (A + 2);
-  const int per = (n + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * per, r1 = min(n, r0 + per);
-  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-    const int a = o / (A + 2), c = o % (A + 2);
-    float s = 0.f;
-    for (int r = r0; r < r1; ++r) {
-      const float gv = a < A ? dlog[(size_t)r * A + a] : dbase[r];
-      if (c == 0) s += gv;
-      else if (c == 1) s += gv * fminf(fmaxf(reward[r], -1.f), 1.f);
-      else if (last_action[r] == c - 2) s += gv;
-    }
-    partial[(size_t)blockIdx.x * nout + o] = s;
+// heads operand Whf [32][576]: row a < A = [Wp[a][0..core) | bp[a] | 0], row A = [Wv | bv | 0]
+__global__ void pack_heads_kernel(const float* __restrict__ wp, const float* __restrict__ bp,
+                                  const float* __restrict__ wv, const float* __restrict__ bv,
+                                  __nv_bfloat16* __restrict__ whf, int A) {
+  const int core = 513 + A;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += gridDim.x * blockDim.x) {
+    const int a = i / kCoreW, j = i % kCoreW;
+    float v = 0.f;
+    if (a < A) v = j < core ? wp[(size_t)a * core + j] : (j == core ? bp[a] : 0.f);
+    else if (a == A) v = j < core ? wv[j] : (j == core ? bv[0] : 0.f);
+    whf[i] = __float2bfloat16_rn(v);
   }
 }
 
@@ -315,56 +227,94 @@ __global__ void __launch_bounds__(512) heads_aux_kernel(const float* __restrict_
 struct FinJob {
   const float* partial;
   float* dst;
-  int kind;        // 0 split-K [splits][Mpad][N] -> torch-layout dst; 1 colsum [ctas][C]; 2 heads-wgrad; 3 heads-aux
-  int L;           // kind 0: layer for torch_w_index
-  int splits;      // kind 0/2: splits, kind 1/3: ctas
-  int M, N, Npad;  // kind 0/2: valid rows / cols, partial row length; kind 1/3: N = width
+  int kind;     // 0 split-K [splits][Mpad][Npad] -> dst[n*M + m] * alpha (transpose to [Cout][K]);
+                // 1 colsum [R][G*C] -> dst[c] = sum_r sum_g; 2 heads split-K routing
+  int splits;   // kind 0/2: splits; kind 1: R (partial rows)
+  int M, N;     // kind 0/2: valid rows (K) / cols (Cout); kind 1: M = G groups, N = C
+  int Npad;
   long long Mpad;
   float alpha;
 };
 struct FinArgs {
-  FinJob job[12];
+  FinJob job[8];
   int njobs;
-  int A, core;
-  float* wp_grad;  // heads routing
+  int A;
+  float* wp_grad;
   float* bp_grad;
   float* wv_grad;
   float* bv_grad;
 };
 
+BP_DEVICE float fin_partial(const FinJob& j, long long i, int r) {
+  if (j.kind == 1) {  // r over rows * groups
+    const int row = r / j.M, grp = r - row * j.M;
+    return j.partial[(long long)row * j.M * j.N + (long long)grp * j.N + i];
+  }
+  const long long m = i / j.N, n = i % j.N;
+  return j.partial[((long long)r * j.Mpad + m) * j.Npad + n];
+}
+
+BP_DEVICE void fin_store(const FinArgs& a, const FinJob& j, long long i, float s) {
+  if (j.kind == 1) {
+    j.dst[i] = s;
+    return;
+  }
+  const long long m = i / j.N, n = i % j.N;
+  s *= j.alpha;
+  if (j.kind == 0) {
+    j.dst[n * j.M + m] = s;
+  } else {  // heads: D[jj][aa], core = 513 + A; row core is the bias (ones) column
+    const int core = 513 + a.A;
+    if (n < a.A) {
+      if (m < core) a.wp_grad[n * core + m] = s;
+      else if (m == core) a.bp_grad[n] = s;
+    } else if (n == a.A) {
+      if (m < core) a.wv_grad[m] = s;
+      else if (m == core) a.bv_grad[0] = s;
+    }
+  }
+}
+
+// Split-K jobs: one warp per output (fixed lane split + fixed shuffle tree) or one
+// thread per output.  Column-sum jobs (thousands of partials, few outputs): one block per
+// output, fixed strided split + fixed shared-memory tree.  All deterministic.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinArgs a) {
   const FinJob& j = a.job[blockIdx.y];
-  const long long total = (j.kind == 0 || j.kind == 2) ? (long long)j.M * j.N : j.N;
+  if (j.kind == 1) {
+    __shared__ float red[256];
+    const int nparts = j.splits * j.M;
+    for (int c = blockIdx.x; c < j.N; c += gridDim.x) {
+      float s = 0.f;
+      for (int r = threadIdx.x; r < nparts; r += 256) s += fin_partial(j, c, r);
+      red[threadIdx.x] = s;
+      __syncthreads();
+      for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) fin_store(a, j, c, red[0]);
+      __syncthreads();
+    }
+    return;
+  }
+  // split-K: one thread per output; consecutive threads read consecutive partial
+  // columns (coalesced), the split loop is unrolled for memory-level parallelism
+  const long long total = (long long)j.M * j.N;
+  const long long pstride = j.Mpad * j.Npad;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    if (j.kind == 0 || j.kind == 2) {
-      const long long m = i / j.N, n = i % j.N;
-      for (int sp = 0; sp < j.splits; ++sp) s += j.partial[((long long)sp * j.Mpad + m) * j.Npad + n];
-      s *= j.alpha;
-      if (j.kind == 0) {
-        j.dst[torch_w_index(j.L, (int)n, (int)m)] = s;
-      } else {  // heads wgrad: D[k][aa] -> dWp[aa][k] / dWv[k]
-        if (n < a.A) a.wp_grad[n * a.core + m] = s;
-        else if (n == a.A) a.wv_grad[m] = s;
-      }
-    } else {
-      for (int c = 0; c < j.splits; ++c) s += j.partial[(long long)c * j.N + i];
-      if (j.kind == 1) {
-        j.dst[i] = s;
-      } else {  // heads aux: o = aa*(A+2) + c
-        const int aa = (int)(i / (a.A + 2)), c = (int)(i % (a.A + 2));
-        float* row = aa < a.A ? a.wp_grad + (size_t)aa * a.core : a.wv_grad;
-        if (c == 0) {
-          if (aa < a.A) a.bp_grad[aa] = s;
-          else a.bv_grad[0] = s;
-        } else if (c == 1) {
-          row[512] = s;
-        } else {
-          row[513 + (c - 2)] = s;
-        }
-      }
+    const long long m = i / j.N, n = i % j.N;
+    const float* p = j.partial + m * j.Npad + n;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int r = 0;
+    for (; r + 4 <= j.splits; r += 4) {
+      s0 += p[(long long)r * pstride];
+      s1 += p[(long long)(r + 1) * pstride];
+      s2 += p[(long long)(r + 2) * pstride];
+      s3 += p[(long long)(r + 3) * pstride];
     }
+    for (; r < j.splits; ++r) s0 += p[(long long)r * pstride];
+    fin_store(a, j, i, (s0 + s1) + (s2 + s3));
   }
 }
 
@@ -376,26 +326,23 @@ struct WgPlan {
   size_t off, floats;
 };
 struct NetPlan {
-  WgPlan wg[5];  // conv1, conv2, conv3, fc, heads
-  size_t colsum_off[4];
-  int colsum_ctas;
-  size_t aux_off;
-  int aux_ctas;
+  WgPlan wg[4];       // conv1, conv2, conv3, heads (fc wgrad writes the grads directly)
+  size_t cs_off[4];   // colsum partials: db1 (conv2 dgrad), db2, db3, dbfc
+  int cs_rows[4], cs_n[4];
   size_t total_floats;
 };
 
-static void make_plan(int n, int A, int sms, NetPlan* P) {
-  const long long rows[5] = {(long long)n * 441, (long long)n * 100, (long long)n * 81, n, n};
-  const int M[5] = {256, 512, 576, 3136, 512};
-  const int BNs[5] = {32, 64, 64, 256, 64};
-  const int Ns[5] = {32, 64, 64, 512, 64};
+static void make_plan(int n, int sms, NetPlan* P) {
+  const long long rows[4] = {(long long)n * 441, (long long)n * 100, (long long)n * 81, n};
+  const int M[4] = {256, 512, 576, kCoreW};
+  const int Ns[4] = {32, 64, 64, 64};
   size_t off = 0;
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < 4; ++i) {
     WgPlan& w = P->wg[i];
     w.m_tiles = (M[i] + 127) / 128;
-    w.n_tiles = Ns[i] / BNs[i];
+    w.n_tiles = 1;
     w.num_kb = (int)((rows[i] + 63) / 64);
-    int sp = (sms + w.m_tiles * w.n_tiles - 1) / (w.m_tiles * w.n_tiles);
+    int sp = (sms + w.m_tiles - 1) / w.m_tiles;
     if (sp > w.num_kb) sp = w.num_kb;
     if (sp < 1) sp = 1;
     w.kb_per = (w.num_kb + sp - 1) / sp;
@@ -406,15 +353,17 @@ static void make_plan(int n, int A, int sms, NetPlan* P) {
     w.floats = (size_t)w.splits * w.Mpad * w.Npad;
     off += (w.floats + 63) & ~size_t(63);
   }
-  P->colsum_ctas = 2 * sms;
-  const int C[4] = {32, 64, 64, 512};
+  // dgrad epilogue column sums: rows = 4 * m_tiles of the producing GEMM, width = its N
+  const long long drows[4] = {(long long)n * 100, (long long)n * 81, n, n};
+  const int dn[4] = {128, 64, 3136, 512};
+  const bool cta_mode[4] = {true, true, false, false};  // producing GEMM has a single N tile
   for (int i = 0; i < 4; ++i) {
-    P->colsum_off[i] = off;
-    off += ((size_t)P->colsum_ctas * C[i] + 63) & ~size_t(63);
+    const long long mt = (drows[i] + 127) / 128;
+    P->cs_rows[i] = (int)(4 * (cta_mode[i] ? (mt < sms ? mt : sms) : mt));
+    P->cs_n[i] = dn[i];
+    P->cs_off[i] = off;
+    off += ((size_t)P->cs_rows[i] * dn[i] + 63) & ~size_t(63);
   }
-  P->aux_ctas = 64;
-  P->aux_off = off;
-  off += ((size_t)P->aux_ctas * (A + 1) * (A + 2) + 63) & ~size_t(63);
   P->total_floats = off;
 }
 
@@ -426,10 +375,8 @@ using namespace bp;
 // Raw engine entry for unit tests: C[M][N] f32 = A . B^T with
 //   a_mn = 0: A stored [M][K] (K-major), 1: A stored [K][M] (MN-major)
 //   b_mn = 0: B stored [N][K],           1: B stored [K][N]
-// M % 128 == 0 (a_mn=0) or M % 64 == 0 (a_mn=1); K % 64 == 0; N in {32, 64, 128, 256} or a
-// multiple of 256 (K-major B) / of 64 (MN-major B).
-extern "C" int bp_gemm_bf16_test(const void* A, const void* B, float* C, int M, int N, int K,
-                                 int a_mn, int b_mn, int splits, void* stream) {
+extern "C" int bp_gemm_bf16_test(const void* A, const void* B, void* C, int M, int N, int K,
+                                 int a_mn, int b_mn, int splits, int out_bf16, void* stream) {
   if (int e = init_driver()) return e;
   cudaStream_t s = (cudaStream_t)stream;
   if (K % 64 || M % 64 || (!a_mn && M % 128) || splits < 1) {
@@ -451,7 +398,7 @@ extern "C" int bp_gemm_bf16_test(const void* A, const void* B, float* C, int M, 
   g.kb_per_split = (g.num_kb + splits - 1) / splits;
   g.N = N;
   g.M = g.m_tiles * 128;
-  g.out_f32 = 1;
+  g.out_f32 = out_bf16 ? 0 : 1;
   g.out = C;
   g.r_img = N;
   g.split_stride = (long long)g.m_tiles * 128 * N;
@@ -481,6 +428,7 @@ extern "C" int bp_gemm_bf16_test(const void* A, const void* B, float* C, int M, 
   BP_GT(64, A_MNMAJOR, B_MNMAJOR, 128)
   BP_GT(256, A_MNMAJOR, B_MNMAJOR, 128)
   BP_GT(64, A_KMAJOR, B_MNMAJOR, 128)
+  BP_GT(128, A_KMAJOR, B_MNMAJOR, 128)
   BP_GT(64, A_MNMAJOR, B_KMAJOR, 128)
 #undef BP_GT
   set_error("gemm_test: combination not instantiated (N=%d a_mn=%d b_mn=%d)", N, a_mn, b_mn);
@@ -504,9 +452,10 @@ extern "C" int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* of
 }
 
 extern "C" size_t bp_atari_workspace_bytes(int num_actions, int max_frames) {
+  (void)num_actions;
   if (init_driver()) return 0;
   NetPlan P;
-  make_plan(max_frames, num_actions, g_num_sms, &P);
+  make_plan(max_frames, g_num_sms, &P);
   return P.total_floats * sizeof(float);
 }
 
@@ -520,30 +469,11 @@ static int check_net(const BpAtariNet* net, int n) {
 
 extern "C" int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stream) {
   if (int e = check_net(net, 1)) return e;
-  const int A = net->num_actions, core = 512 + 1 + A;
   int64_t off[P_COUNT + 1];
-  param_offsets(A, off);
-  PackArgs a;
-  memset(&a, 0, sizeof(a));
-  auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
-  int k = 0;
-  // forward B operands [N][K] from master [K][N]  (2D transpose: P=K, Q=N, R=1)
-  a.job[k++] = {params + off[P_W1], bf(net->w1f), 0, 1, 32, 256, 64, 4};
-  a.job[k++] = {params + off[P_W2], bf(net->w2f), 0, 2, 64, 512, 128, 4};
-  a.job[k++] = {params + off[P_W3], bf(net->w3f), 0, 3, 64, 576, 64, 9};
-  a.job[k++] = {params + off[P_WFC], bf(net->wfcf), 0, 4, 512, 3136, 3136, 1};
-  a.job[k++] = {params + off[P_W2], bf(net->w2d), 1, 2, 64, 512, 128, 4};
-  a.job[k++] = {params + off[P_W3], bf(net->w3d), 1, 3, 64, 576, 64, 9};
-  a.job[k++] = {params + off[P_WFC], bf(net->wfcd), 2, 4, 512, 3136, 3136, 1};
-  a.job[k++] = {nullptr, bf(net->whf), 3, 0, 0, 0, 0, 0};
-  a.job[k++] = {nullptr, bf(net->whd), 4, 0, 0, 0, 0, 0};
-  a.njobs = k;
-  a.wp = params + off[P_WP];
-  a.wv = params + off[P_WV];
-  a.A = A;
-  a.core = core;
-  pack_weights_kernel<<<dim3(148, k), 256, 0, (cudaStream_t)stream>>>(a);
-  return check_launch("pack_weights_kernel");
+  param_offsets(net->num_actions, off);
+  cast_bf16_kernel<<<296, 256, 0, (cudaStream_t)stream>>>(
+      params, reinterpret_cast<__nv_bfloat16*>(net->wbf), off[P_COUNT]);
+  return check_launch("cast_bf16_kernel");
 }
 
 extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
@@ -551,24 +481,28 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
                                 float* logits, float* baseline, void* stream) {
   if (int e = check_net(net, n)) return e;
   cudaStream_t s = (cudaStream_t)stream;
-  const int A = net->num_actions, core = 512 + 1 + A;
+  const int A = net->num_actions;
   int64_t off[P_COUNT + 1];
   param_offsets(A, off);
+  const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
+  auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
-  // 1. frames -> space-to-depth bf16
-  frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, reinterpret_cast<__nv_bfloat16*>(net->x0));
+  // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
+  frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, bf(net->x0), reward, last_action, bf(net->core), A);
   if ((rc = check_launch("frames_s2d_kernel"))) return rc;
+  pack_heads_kernel<<<36, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
+                                       params + off[P_BV], bf(net->whf), A);
+  if ((rc = check_launch("pack_heads_kernel"))) return rc;
   CUtensorMap ta, tb;
-  // 2. conv1: X0 [n*441, 64] x w1f [32, 256] -> relu(./255 + b1) -> X1 (s2d-2 layout)
+  // 2. conv1: X0 [n*441, 64] x W1 [32, 256] -> relu(./255 + b1) -> X1 (s2d-2 layout)
   {
     const long long R = (long long)n * 441;
     if ((rc = make_tmap(&ta, net->x0, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->w1f, 32, 256, 64, 32, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W1], 32, 256, 64, 32, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 4;
-    g.a_cb = 1;
     const int offs[4] = {0, 1, 21, 22};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = offs[i];
     g.N = 32;
@@ -577,6 +511,7 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bias = params + off[P_B1];
     g.relu = 1;
     g.out = net->x1;
+    g.bits_out = reinterpret_cast<uint32_t*>(net->m1);
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
     if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
@@ -585,7 +520,7 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
   {
     const long long R = (long long)n * 100;
     if ((rc = make_tmap(&ta, net->x1, R, 128, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->w2f, 64, 512, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
@@ -598,6 +533,7 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bias = params + off[P_B2];
     g.relu = 1;
     g.out = net->x2;
+    g.bits_out = reinterpret_cast<uint32_t*>(net->m2);
     g.gh = 10; g.gw = 10; g.vh = 9; g.vw = 9;
     g.r_img = 81 * 64; g.r_y = 9 * 64; g.r_x = 64;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
@@ -606,12 +542,11 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
   {
     const long long R = (long long)n * 81;
     if ((rc = make_tmap(&ta, net->x2, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->w3f, 64, 576, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 9;
-    g.a_cb = 1;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) g.a_row_off[dy * 3 + dx] = dy * 9 + dx;
     g.N = 64;
@@ -619,47 +554,42 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bias = params + off[P_B3];
     g.relu = 1;
     g.out = net->x3;
+    g.bits_out = reinterpret_cast<uint32_t*>(net->m3);
     g.gh = 9; g.gw = 9; g.vh = 7; g.vw = 7;
     g.r_img = 3136; g.r_y = 7 * 64; g.r_x = 64;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 5. fc: X3 [n, 3136] x wfcf [512, 3136] -> H = relu(. + bfc) [n, 512]
+  // 5. fc: X3 [n, 3136] x Wfc [512, 3136] -> core[:, :512] = relu(. + bfc)
   {
     if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->wfcf, 512, 3136, 64, 256, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (n + 127) / 128;
-    g.n_tiles = 2;
+    g.n_tiles = 8;
     g.num_kb = g.kb_per_split = 49;
     g.a_cb = 49;
     g.N = 512;
     g.M = n;
     g.bias = params + off[P_BFC];
     g.relu = 1;
-    g.out = net->h;
-    g.r_img = 512;
-    if ((rc = launch_gemm<256, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.out = net->core;
+    g.bits_out = reinterpret_cast<uint32_t*>(net->mc);
+    g.r_img = kCoreW;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 6. heads: H [n, 512] x whf [32, 512] -> logits [n, A], baseline [n]
+  // 6. heads: core [n, 576] x Whf [32, 576] -> logits [n, A], baseline [n]
   {
-    if ((rc = make_tmap(&ta, net->h, n, 512, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->whf, 32, 512, 64, 32, 128))) return rc;
+    if ((rc = make_tmap(&ta, net->core, n, kCoreW, 64, 128, 128))) return rc;
+    if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 32, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (n + 127) / 128;
     g.n_tiles = 1;
-    g.num_kb = g.kb_per_split = 8;
-    g.a_cb = 8;
+    g.num_kb = g.kb_per_split = kCoreW / 64;
+    g.a_cb = kCoreW / 64;
     g.N = 32;
     g.M = n;
     g.heads = 1;
     g.A = A;
-    g.core = core;
-    g.wp = params + off[P_WP];
-    g.bp = params + off[P_BP];
-    g.wv = params + off[P_WV];
-    g.bv = params + off[P_BV];
-    g.reward = reward;
-    g.last_action = last_action;
     g.logits = logits;
     g.baseline = baseline;
     if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
@@ -670,43 +600,48 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
 extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits,
                                  const float* d_baseline, const float* reward,
                                  const int64_t* last_action, float* grads, void* stream) {
+  (void)reward;
+  (void)last_action;  // (their contribution to the heads gradient comes from the augmented core)
   if (int e = check_net(net, n)) return e;
   cudaStream_t s = (cudaStream_t)stream;
-  const int A = net->num_actions, core = 512 + 1 + A;
+  const int A = net->num_actions;
   int64_t off[P_COUNT + 1];
   param_offsets(A, off);
   NetPlan P;
-  make_plan(n, A, g_num_sms, &P);
+  make_plan(n, g_num_sms, &P);
   if (P.total_floats * sizeof(float) > net->ws_bytes) {
     set_error("atari backward: workspace %zu < %zu bytes", net->ws_bytes, P.total_floats * sizeof(float));
     return BP_ERR_ARG;
   }
   float* ws = reinterpret_cast<float*>(net->ws);
+  const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
   CUtensorMap ta, tb;
   // 1. G = [d_logits | d_baseline | 0] bf16
   pack_g_kernel<<<(n * 8 + 255) / 256, 256, 0, s>>>(d_logits, d_baseline, bf(net->g), n, A);
   if ((rc = check_launch("pack_g_kernel"))) return rc;
-  // 2. heads dgrad: d_fc = (G [n,64] x whd [512,64]^T) * (H > 0)
+  // 2. heads dgrad: d_fc = (G [n,64] x Whf[:, :512]) * (h > 0); colsum -> d bfc
   {
     if ((rc = make_tmap(&ta, net->g, n, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->whd, 512, 64, 64, 256, 128))) return rc;
+    if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 64, 128))) return rc;  // MN-major, rows >= 32 OOB = 0
     GemmArgs g = base_args();
     g.m_tiles = (n + 127) / 128;
-    g.n_tiles = 2;
+    g.n_tiles = 8;
     g.num_kb = g.kb_per_split = 1;
     g.N = 512;
     g.M = n;
-    g.mask = bf(net->h);
+    g.mask_bits = reinterpret_cast<const uint32_t*>(net->mc);
+    g.mask_ld = kCoreW;
     g.out = net->d_fc;
     g.r_img = 512;
-    if ((rc = launch_gemm<256, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.colsum = ws + P.cs_off[3];
+    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 3. fc dgrad: d_pre3 (conv3 9x9 grid) = (d_fc [n,512] x wfcd [3136,512]^T) * (X3 > 0)
+  // 3. fc dgrad: d_pre3 (conv3 9x9 grid) = (d_fc [n,512] x Wfc [512,3136]) * (X3 > 0); colsum -> d b3
   {
     if ((rc = make_tmap(&ta, net->d_fc, n, 512, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->wfcd, 3136, 512, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (n + 127) / 128;
     g.n_tiles = 49;
@@ -714,52 +649,59 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.a_cb = 8;
     g.N = 3136;
     g.M = n;
-    g.mask = bf(net->x3);
+    g.mask_bits = reinterpret_cast<const uint32_t*>(net->m3);
     g.out = net->d_pre3;
     g.r_img = 81 * 64;
     g.cdiv = 64; g.cq = 7; g.cs1 = 9 * 64; g.cs2 = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.colsum = ws + P.cs_off[2];
+    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 4. conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] w3d * (X2 > 0)
+  // 4. conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
   {
     const long long R = (long long)n * 81;
     if ((rc = make_tmap(&ta, net->d_pre3, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->w3d, 64, 576, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 9;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) g.a_row_off[dy * 3 + dx] = -(dy * 9 + dx);
+    g.b_kb_per_tap = 1;
+    g.b_tap_stride = 64;
     g.N = 64;
     g.M = (int)R;
-    g.mask = bf(net->x2);
+    g.mask_bits = reinterpret_cast<const uint32_t*>(net->m2);
     g.out = net->d_pre2;
     g.gh = 9; g.gw = 9; g.vh = 9; g.vw = 9;
     g.r_img = 100 * 64; g.r_y = 10 * 64; g.r_x = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.colsum = ws + P.cs_off[1];
+    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 5. conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] w2d * (X1 > 0), inverse s2d
+  // 5. conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
   {
     const long long R = (long long)n * 100;
     if ((rc = make_tmap(&ta, net->d_pre2, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->w2d, 128, 256, 64, 128, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 4;
     const int offs[4] = {0, 1, 10, 11};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = -offs[i];
+    g.b_kb_per_tap = 1;
+    g.b_tap_stride = 128;
     g.N = 128;
     g.M = (int)R;
-    g.mask = bf(net->x1);
+    g.mask_bits = reinterpret_cast<const uint32_t*>(net->m1);
     g.out = net->d_pre1;
     g.gh = 10; g.gw = 10; g.vh = 10; g.vw = 10;
     g.r_img = 441 * 32; g.r_y = 2 * 21 * 32; g.r_x = 2 * 32;
     g.cdiv = 32; g.cq = 2; g.cs1 = 21 * 32; g.cs2 = 32;
-    if ((rc = launch_gemm<128, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.colsum = ws + P.cs_off[0];
+    if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 6. weight gradients: D[(tap, cin)][cout] = sum_rows X[row + off_tap][cin] dY[row][cout]
+  // 6. weight gradients
   auto wgrad = [&](int i, const void* X, long long xrows, int xcols, int atoms_per_shift, int nshifts,
                    const int* offs, const void* dY, int ncols) -> int {
     const WgPlan& w = P.wg[i];
@@ -783,13 +725,9 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     if (ncols == 32) {
       if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
       return launch_gemm<32, A_MNMAJOR, B_MNMAJOR, 64>(g, ta, tb, s);
-    } else if (ncols == 64) {
-      if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
-      return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
-    } else {
-      if ((r = make_tmap(&tb, dY, xrows, 512, 64, 64, 128))) return r;
-      return launch_gemm<256, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
     }
+    if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
+    return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
   };
   {
     const int o1[4] = {0, 1, 21, 22};
@@ -801,53 +739,55 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
       for (int dx = 0; dx < 3; ++dx) o3[dy * 3 + dx] = dy * 9 + dx;
     if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
     const int o0[1] = {0};
-    if ((rc = wgrad(3, net->x3, n, 3136, 49, 1, o0, net->d_fc, 512))) return rc;
-    if ((rc = wgrad(4, net->h, n, 512, 8, 1, o0, net->g, 64))) return rc;
+    if ((rc = wgrad(3, net->core, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
   }
-  // 7. bias gradients (column sums) + heads auxiliary gradients
+  // fc weight gradient with swapped roles: D[o][k] = sum_n d_fc[n][o] X3[n][k] -> grads, no split
   {
-    ColsumArgs c;
-    memset(&c, 0, sizeof(c));
-    c.ctas = P.colsum_ctas;
-    c.job[0] = {bf(net->d_pre1), (long long)n * 441, 32, ws + P.colsum_off[0]};
-    c.job[1] = {bf(net->d_pre2), (long long)n * 100, 64, ws + P.colsum_off[1]};
-    c.job[2] = {bf(net->d_pre3), (long long)n * 81, 64, ws + P.colsum_off[2]};
-    c.job[3] = {bf(net->d_fc), (long long)n, 512, ws + P.colsum_off[3]};
-    colsum_kernel<<<dim3(c.ctas, 4), 256, 0, s>>>(c);
-    if ((rc = check_launch("colsum_kernel"))) return rc;
-    heads_aux_kernel<<<P.aux_ctas, 512, 0, s>>>(d_logits, d_baseline, reward, last_action, n, A,
-                                                 ws + P.aux_off);
-    if ((rc = check_launch("heads_aux_kernel"))) return rc;
+    if ((rc = make_tmap(&ta, net->d_fc, n, 512, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, net->x3, n, 3136, 64, 64, 128))) return rc;
+    GemmArgs g = base_args();
+    g.m_tiles = 4;
+    g.n_tiles = 49;
+    g.num_kb = g.kb_per_split = (n + 63) / 64;
+    g.a_atoms_per_shift = 8;
+    g.a_nshifts = 1;
+    g.N = 3136;
+    g.M = 512;
+    g.out_f32 = 1;
+    g.out = grads + off[P_WFC];
+    g.r_img = 3136;
+    if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 8. deterministic finalize into the f32 gradient buffer
+  // 7. deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
   {
     FinArgs f;
     memset(&f, 0, sizeof(f));
-    const int pw[4] = {P_W1, P_W2, P_W3, P_WFC};
-    const int Mv[4] = {256, 512, 576, 3136};
-    const int Nv[4] = {32, 64, 64, 512};
+    const int pw[3] = {P_W1, P_W2, P_W3};
+    const int Mv[3] = {256, 512, 576};
+    const int Nv[3] = {32, 64, 64};
     int k = 0;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 3; ++i) {
       const WgPlan& w = P.wg[i];
-      f.job[k++] = {ws + w.off, grads + off[pw[i]], 0, i + 1, w.splits, Mv[i], Nv[i], w.Npad, w.Mpad,
+      f.job[k++] = {ws + w.off, grads + off[pw[i]], 0, w.splits, Mv[i], Nv[i], w.Npad, w.Mpad,
                     i == 0 ? 1.f / 255.f : 1.f};
     }
     {
-      const WgPlan& w = P.wg[4];
-      f.job[k++] = {ws + w.off, nullptr, 2, 0, w.splits, 512, A + 1, w.Npad, w.Mpad, 1.f};
+      const WgPlan& w = P.wg[3];
+      f.job[k++] = {ws + w.off, nullptr, 2, w.splits, 513 + A + 1, A + 1, w.Npad, w.Mpad, 1.f};
     }
+    // biases: db1 from conv2 dgrad (width 128 = 4 groups of 32), db2, db3 (3136 = 49 x 64), dbfc
     const int pb[4] = {P_B1, P_B2, P_B3, P_BFC};
+    const int C[4] = {32, 64, 64, 512};
     for (int i = 0; i < 4; ++i)
-      f.job[k++] = {ws + P.colsum_off[i], grads + off[pb[i]], 1, 0, P.colsum_ctas, 0, Nv[i], 0, 0, 1.f};
-    f.job[k++] = {ws + P.aux_off, nullptr, 3, 0, P.aux_ctas, 0, (A + 1) * (A + 2), 0, 0, 1.f};
+      f.job[k++] = {ws + P.cs_off[i], grads + off[pb[i]], 1, P.cs_rows[i], P.cs_n[i] / C[i], C[i], 0, 0,
+                    1.f};
     f.njobs = k;
     f.A = A;
-    f.core = core;
     f.wp_grad = grads + off[P_WP];
     f.bp_grad = grads + off[P_BP];
     f.wv_grad = grads + off[P_WV];
     f.bv_grad = grads + off[P_BV];
-    finalize_kernel<<<dim3(64, k), 256, 0, s>>>(f);
+    finalize_kernel<<<dim3(148, k), 256, 0, s>>>(f);
     if ((rc = check_launch("finalize_kernel"))) return rc;
   }
   return BP_OK;

@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kOptThreads)
     rmsprop_kernel(float* __restrict__ p, float* __restrict__ g, float* __restrict__ s, int64_t n,
                    const double* __restrict__ sumsq, float max_norm, int mode, float lr_host,
                    const float* __restrict__ lr_dev, float alpha, float eps, int write_grads,
-                   float* __restrict__ norm_out, unsigned* status) {
+                   float* __restrict__ norm_out, __nv_bfloat16* __restrict__ mirror,
+                   unsigned* status) {
   const ClipScale cs = clip_scale(sumsq, max_norm, mode);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (norm_out) *norm_out = (float)sqrt(*sumsq);
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(kOptThreads)
   const int64_t tid = (int64_t)blockIdx.x * kOptThreads + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kOptThreads;
   const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
-                     reinterpret_cast<uintptr_t>(s)) & 15u) == 0;
+                     reinterpret_cast<uintptr_t>(s)) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(mirror) & 7u) == 0;
   int64_t start = 0;
   if (vec) {
     const int64_t n4 = n >> 2;
@@ -115,6 +117,11 @@ __global__ void __launch_bounds__(kOptThreads)
       p4[i] = pv;
       s4[i] = sv;
       if (write_grads) g4[i] = gv;
+      if (mirror) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(pv.x, pv.y), hi = __floats2bfloat162_rn(pv.z, pv.w);
+        reinterpret_cast<uint2*>(mirror)[i] =
+            make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      }
     }
     start = n4 << 2;
   }
@@ -125,6 +132,7 @@ __global__ void __launch_bounds__(kOptThreads)
     p[i] = pv;
     s[i] = sv;
     if (write_grads) g[i] = gv;
+    if (mirror) mirror[i] = __float2bfloat16_rn(pv);
   }
 }
 
@@ -153,8 +161,8 @@ extern "C" int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* work
 extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t n,
                                    const double* sumsq, float max_norm, int clip_mode, float lr,
                                    const float* lr_dev, float alpha, float eps,
-                                   int write_clipped_grads, float* norm_out, unsigned* status,
-                                   void* stream) {
+                                   int write_clipped_grads, float* norm_out, void* bf16_mirror,
+                                   unsigned* status, void* stream) {
   if (n < 0 || !params || !grads || !square_avg || !sumsq || clip_mode < 0 || clip_mode > 2) {
     set_error("rmsprop_clip: bad args");
     return BP_ERR_ARG;
@@ -163,6 +171,6 @@ extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_av
   int grid = (int)(want < 1 ? 1 : (want > 4 * 148 ? 4 * 148 : want));
   rmsprop_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(
       params, grads, square_avg, n, sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps,
-      write_clipped_grads, norm_out, status);
+      write_clipped_grads, norm_out, reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status);
   return check_launch("rmsprop_kernel");
 }

@@ -44,7 +44,9 @@ struct GemmArgs {
   float alpha;           // v = alpha * acc (+ bias)
   const float* bias;     // [N] or null
   int relu;              // apply max(0, .)
-  const __nv_bfloat16* mask;  // relu-backward mask source, same (m, n) index, ld N; null = none
+  const uint32_t* mask_bits;  // relu-backward mask: bit (m * mask_ld + n) of this bit array; null = none
+  int mask_ld;                // element row pitch of the masked activation (0 -> N)
+  uint32_t* bits_out;         // forward: relu mask bits of the stored output, word = element offset / 32
   int out_f32;           // 1: f32 output, 0: bf16
   void* out;
   long long split_stride;  // elements between split partial outputs
@@ -54,17 +56,17 @@ struct GemmArgs {
   // column map: C(n) = ((n/cdiv)/cq)*cs1 + ((n/cdiv)%cq)*cs2 + n%cdiv
   int cdiv, cq;
   long long cs1, cs2;
-  // AtariNet heads epilogue (heads != 0): columns j < A are policy logits, j == A
-  // the baseline; adds bias + W[:, 512] * clip(reward) + W[:, 513 + last_action]
-  int heads, A, core;          // core = 512 + 1 + A (row length of Wp / Wv)
-  const float* wp;             // [A][core]  f32 master policy weight
-  const float* bp;             // [A]
-  const float* wv;             // [core]
-  const float* bv;             // [1]
-  const float* reward;         // [M]
-  const int64_t* last_action;  // [M]
-  float* logits;               // [M][A]
-  float* baseline;             // [M]
+  // B MN-major addressing: box x = (kb / b_kb_per_tap) * b_tap_stride + n0 + 64 j,
+  //                          box y = (kb % b_kb_per_tap) * 64
+  int b_kb_per_tap;
+  int b_tap_stride;
+  // bias-gradient column sums of the stored (post-mask) values, deterministic:
+  // colsum[(mt * 4 + epilogue_warp) * N + n] = sum over that warp's 32 rows (splits == 1)
+  float* colsum;
+  // AtariNet heads epilogue (heads != 0): column j < A -> logits[m][j], j == A -> baseline[m]
+  int heads, A;
+  float* logits;   // [M][A] f32
+  float* baseline; // [M] f32
 };
 
 template <int BN, int AM, int BM, int BSWZ>
@@ -106,11 +108,16 @@ BP_DEVICE void issue_loads(const GemmArgs& g, const CUtensorMap* tmA, const CUte
   }
   if constexpr (BM == B_KMAJOR) {
     sm100::tma_load_2d(sb, tmB, bar, kb * 64, nt * BN);
-  } else if constexpr (BSWZ == 64) {
-    sm100::tma_load_2d(sb, tmB, bar, nt * BN, kb * 64);
   } else {
+    const int tap = kb / g.b_kb_per_tap;
+    const int x0 = tap * g.b_tap_stride + nt * BN;
+    const int y = (kb - tap * g.b_kb_per_tap) * 64;
+    if constexpr (BSWZ == 64) {
+      sm100::tma_load_2d(sb, tmB, bar, x0, y);
+    } else {
 #pragma unroll
-    for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, tmB, bar, nt * BN + j * 64, kb * 64);
+      for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, tmB, bar, x0 + j * 64, y);
+    }
   }
 }
 
@@ -131,33 +138,35 @@ BP_DEVICE uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// one row x 32 consecutive columns of the tile
-BP_DEVICE void heads_epilogue(const GemmArgs& g, int m, float (&v)[32]) {
-  const float r = fminf(fmaxf(__ldg(g.reward + m), -1.f), 1.f);
-  const int la = (int)__ldg(g.last_action + m);
-  const bool la_ok = la >= 0 && la < g.A;
-  float bsum = 0.f;
+// lane j ends with sum over the warp's 32 lanes of v[j] (31 shuffles, fixed order)
+BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {  // compile-time indices keep v[] in registers
-    if (j < g.A) {
-      const float* w = g.wp + (size_t)j * g.core;
-      float x = v[j] + __ldg(g.bp + j) + __ldg(w + 512) * r;
-      if (la_ok) x += __ldg(w + 513 + la);
-      g.logits[(size_t)m * g.A + j] = x;
-    } else if (j == g.A) {
-      bsum = v[j];
+  for (int k = 16; k >= 1; k >>= 1) {
+    const bool upper = (lane & k) != 0;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const float send = upper ? v[i] : v[i + k];
+      const float keep = upper ? v[i + k] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
     }
   }
-  float b = bsum + __ldg(g.bv) + __ldg(g.wv + 512) * r;
-  if (la_ok) b += __ldg(g.wv + 513 + la);
-  g.baseline[m] = b;
+  return v[0];
 }
 
+// one row x 32 consecutive columns of the tile (called by all 32 lanes of an epilogue warp)
+// mkw: the prefetched relu-mask word of this row chunk (when g.mask_bits);
+// csum_acc: per-CTA running column sum for this lane's column (null: per-tile partial rows)
 BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
-                              int sp, float (&v)[32]) {
-  if (!row_ok) return;
+                              int sp, int mt, int ew, int lane, float (&v)[32], uint32_t mkw,
+                              float* csum_acc) {
   if (g.heads) {
-    heads_epilogue(g, m, v);
+    if (row_ok) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {  // compile-time indices keep v[] in registers
+        if (n0 + j < g.A) g.logits[(size_t)m * g.A + n0 + j] = v[j];
+        else if (n0 + j == g.A) g.baseline[m] = v[j];
+      }
+    }
     return;
   }
   if (g.alpha != 1.f) {
@@ -172,30 +181,42 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
   }
-  if (g.mask) {
-    const uint4* mp = reinterpret_cast<const uint4*>(g.mask + (size_t)m * g.N + n0);
+  if (g.mask_bits && row_ok) {
+    const uint32_t w = mkw;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 w = __ldg(mp + q);
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&w);
+    for (int i = 0; i < 32; ++i)
+      if (!((w >> i) & 1u)) v[i] = 0.f;
+  }
+  if (row_ok) {
+    const int qd = n0 / g.cdiv;
+    const long long cbase = (long long)(qd / g.cq) * g.cs1 + (long long)(qd % g.cq) * g.cs2 + (n0 % g.cdiv);
+    const long long off = rbase + cbase + (long long)sp * g.split_stride;
+    if (g.bits_out) {
+      uint32_t bits = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (!(__bfloat162float(h[i]) > 0.f)) v[q * 8 + i] = 0.f;
+      for (int i = 0; i < 32; ++i) bits |= (v[i] > 0.f ? 1u : 0u) << i;
+      g.bits_out[off >> 5] = bits;
+    }
+    if (g.out_f32) {
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out) + off);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                          pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
     }
   }
-  const int qd = n0 / g.cdiv;
-  const long long cbase = (long long)(qd / g.cq) * g.cs1 + (long long)(qd % g.cq) * g.cs2 + (n0 % g.cdiv);
-  const long long off = rbase + cbase + (long long)sp * g.split_stride;
-  if (g.out_f32) {
-    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
+  if (g.colsum) {  // warp-uniform branch
+    if (!row_ok) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  } else {
-    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out) + off);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                        pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    const float sum = warp_transpose_sum(v, lane);
+    if (csum_acc) *csum_acc += sum;
+    else g.colsum[(size_t)(mt * 4 + ew) * g.N + n0 + lane] = sum;
   }
 }
 
@@ -285,8 +306,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
+    constexpr int NCH = BN / 32;
     int acc = 0;
     uint32_t aphase = 0;
+    // bias-gradient column sums: accumulated per CTA when every tile covers the same columns
+    const bool cta_colsum = g.colsum && g.n_tiles == 1 && g.splits == 1;
+    float csum[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) csum[c] = 0.f;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int mt, nt, sp;
       tile_coords(g, tile, mt, nt, sp);
@@ -304,23 +331,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         rbase = (long long)img * g.r_img + (long long)(y / g.sy) * g.r_y + (long long)(x / g.sx) * g.r_x +
                 (long long)((y % g.sy) * g.sx + (x % g.sx)) * g.r_sub;
       }
+      // prefetch the tile's relu-mask words before waiting for the accumulator (overlaps the MMAs)
+      uint32_t mk[NCH];
+      if (g.mask_bits && row_ok) {
+        const uint32_t* mp = g.mask_bits + (((size_t)m * (g.mask_ld ? g.mask_ld : g.N) + nt * BN) >> 5);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) mk[c] = __ldg(mp + c);
+      }
       sm100::mbar_wait(&tfull[acc], aphase);
       sm100::tc_fence_after();
       const bool has_k = (sp * g.kb_per_split) < g.num_kb;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
         uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c + ((uint32_t)(ew * 32) << 16), r);
+        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
         sm100::tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(r[i]) : 0.f;
-        epilogue_chunk(g, rbase, row_ok, m, nt * BN + c, sp, v);
+        epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, mk[c],
+                       cta_colsum ? &csum[c] : nullptr);
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (cta_colsum) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) g.colsum[(size_t)(blockIdx.x * 4 + ew) * g.N + c * 32 + lane] = csum[c];
     }
   }
   __syncthreads();

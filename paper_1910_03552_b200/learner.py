@@ -58,9 +58,57 @@ class FusedLearner:
         self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
         self.pg = process_group
         model.buffers_for(self.n)
+        # CUDA graphs: one captured step per (batch buffer set, optimizer); see step()
+        self.use_graphs = True
+        self.kernels_per_step = 0
+        self._graphs: dict = {}
+        self._seen: set = set()
+
+    def _graph_key(self, batch, optimizer):
+        keys = ("frame", "reward", "done", "policy_logits", "action", "last_action")
+        return tuple(batch[k].data_ptr() for k in keys) + (id(optimizer),)
 
     def step(self, batch, optimizer=None, scheduler=None):
-        """Enqueue one learner step on the current stream; returns the device loss vector."""
+        """Enqueue one learner step on the current stream; returns the device loss vector.
+
+        With `use_graphs` (default) the whole step -- forward, fused loss,
+        backward, all-reduce, clip + RMSProp: ~23 kernels -- is captured once per
+        set of batch buffers (e.g. the two DeviceInfeed slots) as a CUDA graph and
+        replayed, so host launch overhead leaves the critical path.  The first
+        call per buffer set runs eagerly (warm-up), the second captures.
+        """
+        graphable = (self.use_graphs and self.pg is None and
+                     (optimizer is None or (isinstance(optimizer, RMSprop) and
+                                            optimizer.flat_params.data_ptr() ==
+                                            self.model.flat_params.data_ptr())))
+        if graphable:
+            key = self._graph_key(batch, optimizer)
+            g = self._graphs.get(key)
+            if g is None and key in self._seen:
+                optimizer and optimizer.sync_lr()
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                c0 = N.lib().bp_launch_count()
+                with torch.cuda.graph(g, stream=side):
+                    self._step_eager(batch, optimizer)
+                self.kernels_per_step = int(N.lib().bp_launch_count() - c0)
+                torch.cuda.current_stream().wait_stream(side)
+                self._graphs[key] = g
+            if g is not None:
+                if optimizer is not None:
+                    optimizer.sync_lr()
+                g.replay()
+                if scheduler is not None:
+                    scheduler.step()
+                return self.losses
+            self._seen.add(key)
+        self._step_eager(batch, optimizer)
+        if scheduler is not None:
+            scheduler.step()
+        return self.losses
+
+    def _step_eager(self, batch, optimizer=None):
         m, T, B, n = self.model, self.T, self.B, self.n
         frames = batch["frame"]
         if tuple(frames.shape[:2]) != (T + 1, B):
@@ -68,9 +116,10 @@ class FusedLearner:
         A = m.num_actions
         reward = batch["reward"]
         last_action = batch["last_action"]
-        # 1. forward
+        # 1. forward (the bf16 operand mirror is refreshed by the fused optimiser below)
         m._forward_kernels(frames.reshape(n, *m.observation_shape), reward.reshape(n),
-                           last_action.reshape(n), logits=self.logits, baseline=self.baseline)
+                           last_action.reshape(n), logits=self.logits, baseline=self.baseline,
+                           repack=False)
         # 2. fused V-trace + losses + gradients w.r.t. logits / baseline
         self.loss(self.logits[:T * B].view(T, B, A), self.baseline.view(T + 1, B),
                   batch["policy_logits"][1:], batch["action"][1:], reward[1:], batch["done"][1:],
@@ -86,15 +135,15 @@ class FusedLearner:
         # 5. clip + RMSProp
         if optimizer is not None:
             if isinstance(optimizer, RMSprop) and optimizer.flat_params.data_ptr() == m.flat_params.data_ptr():
-                optimizer.step(max_norm=self.max_norm)
+                optimizer.step(max_norm=self.max_norm, mirror=m.flat_bf16)  # params + bf16 mirror
+                m.mirror_fresh = True
             else:  # any torch optimiser: device-side norm + clip, then its own step
                 ss = torch.zeros(1, dtype=torch.float64, device=m.flat_grads.device)
                 sumsq_(m.flat_grads, ss)
                 coef = torch.clamp(self.max_norm / (ss.sqrt().float() + 1e-6), max=1.0)
                 m.flat_grads.mul_(coef)
                 optimizer.step()
-        if scheduler is not None:
-            scheduler.step()
+                m.mirror_fresh = False
         return self.losses
 
     def stats(self, batch, losses=None):
@@ -133,3 +182,49 @@ def learn(flags, actor_model, model, batch, initial_agent_state, optimizer, sche
         if actor_model is not None and actor_model is not model:
             actor_model.load_state_dict(model.state_dict())
         return stats
+
+
+class DeviceInfeed:
+    """Double-buffered pinned-host -> HBM batch infeed on a side stream.
+
+    Next-row item of SURVEY 8f-2 (the reference stacks host rollouts with
+    np.stack, rollout.py:116-144, and the learner reads them from host memory):
+    `put(host_batch)` enqueues the H2D copies of the NEXT batch on a copy
+    stream while the current learner step runs; `get()` makes the compute
+    stream wait for that copy and returns the device batch.
+    """
+
+    def __init__(self, like: dict, device=None, depth: int = 2):
+        self.device = torch.device(device or "cuda")
+        self.depth = depth
+        self.slots = [{k: torch.empty(v.shape, dtype=v.dtype, device=self.device)
+                       for k, v in like.items()} for _ in range(depth)]
+        self.events = [torch.cuda.Event() for _ in range(depth)]
+        self.freed = [torch.cuda.Event() for _ in range(depth)]
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.head = 0  # next slot to fill
+        self.tail = 0  # next slot to consume
+        self.bytes_per_batch = sum(v.numel() * v.element_size() for v in like.values())
+
+    def put(self, host_batch: dict) -> None:
+        slot = self.head % self.depth
+        with torch.cuda.stream(self.stream):
+            if self.head >= self.depth:
+                self.stream.wait_event(self.freed[slot])  # consumer done with this slot
+            for k, v in host_batch.items():
+                self.slots[slot][k].copy_(v, non_blocking=True)
+            self.events[slot].record(self.stream)
+        self.head += 1
+
+    def get(self) -> dict:
+        if self.tail >= self.head:
+            raise RuntimeError("DeviceInfeed.get() without a pending put()")
+        slot = self.tail % self.depth
+        torch.cuda.current_stream(self.device).wait_event(self.events[slot])
+        self.tail += 1
+        return self.slots[slot]
+
+    def release(self) -> None:
+        """Mark the most recently consumed slot reusable (after its step was enqueued)."""
+        slot = (self.tail - 1) % self.depth
+        self.freed[slot].record(torch.cuda.current_stream(self.device))

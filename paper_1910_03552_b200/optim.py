@@ -50,13 +50,13 @@ def rmsprop_clip_(params: torch.Tensor, grads: torch.Tensor, square_avg: torch.T
                   sumsq: torch.Tensor, *, lr: float, alpha: float, eps: float, max_norm: float,
                   clip_mode: str = "torch", lr_dev: torch.Tensor | None = None,
                   write_clipped_grads: bool = True, norm_out: torch.Tensor | None = None,
-                  status=None) -> None:
+                  mirror: torch.Tensor | None = None, status=None) -> None:
     """In-place clip + RMSProp over flat buffers, norm read from `sumsq` on device."""
     sw = status if status is not None else status_word(params.device)
     N.check(N.lib().bp_rmsprop_clip_f32(
         N.ptr(params), N.ptr(grads), N.ptr(square_avg), params.numel(), N.ptr(sumsq),
         float(max_norm), CLIP_MODES[clip_mode], float(lr), N.ptr(lr_dev), float(alpha),
-        float(eps), int(write_clipped_grads), N.ptr(norm_out), sw.ptr(),
+        float(eps), int(write_clipped_grads), N.ptr(norm_out), N.ptr(mirror), sw.ptr(),
         N.stream_handle(params.device)), "bp_rmsprop_clip_f32")
 
 
@@ -127,6 +127,8 @@ class RMSprop(torch.optim.Optimizer):
         self._sumsq = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.norm = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.lr_dev = torch.full((1,), float(lr), dtype=torch.float32, device=self.device)
+        self._lr_host = float(lr)
+        self._sumsq_zero = False
         self.clip_mode = clip_mode
         off = 0
         for p in plist:  # expose torch-style state views
@@ -142,21 +144,30 @@ class RMSprop(torch.optim.Optimizer):
     def zero_grad(self, set_to_none: bool = False):
         self.flat_grads.zero_()
 
+    def sync_lr(self) -> None:
+        """Mirror param_groups[0]["lr"] (edited by LR schedulers) into the device scalar
+        the update kernel reads; called outside CUDA-graph replays."""
+        lr = self.param_groups[0]["lr"]
+        if lr != self._lr_host:
+            self.lr_dev.fill_(lr)
+            self._lr_host = lr
+
     @torch.no_grad()
-    def step(self, closure=None, max_norm: float | None = None):
+    def step(self, closure=None, max_norm: float | None = None, mirror: torch.Tensor | None = None):
         loss = closure() if closure is not None else None
-        # an LR scheduler edits param_groups[0]["lr"]; mirror it on the device
-        self.lr_dev.fill_(self.param_groups[0]["lr"])
+        if not torch.cuda.is_current_stream_capturing():
+            self.sync_lr()
         mode = self.clip_mode if max_norm is not None else "none"
         if mode != "none":
             sumsq_(self.flat_grads, self._sumsq)
-        else:
+        elif not self._sumsq_zero:
             self._sumsq.zero_()
+        self._sumsq_zero = mode == "none"
         g = self.param_groups[0]
         rmsprop_clip_(self.flat_params, self.flat_grads, self.square_avg, self._sumsq,
                       lr=g["lr"], alpha=g["alpha"], eps=g["eps"],
                       max_norm=float(max_norm or 0.0), clip_mode=mode, lr_dev=self.lr_dev,
-                      norm_out=self.norm)
+                      norm_out=self.norm, mirror=mirror)
         return loss
 
 

@@ -51,7 +51,7 @@ def _gpu_masks(net, n):
     m1 = x1.permute(0, 5, 1, 3, 2, 4).reshape(n, 32, 20, 20) > 0
     m2 = t["x2"][: n * 81].float().cpu().view(n, 9, 9, 64).permute(0, 3, 1, 2) > 0
     m3 = t["x3"][:n].float().cpu().view(n, 7, 7, 64).permute(0, 3, 1, 2) > 0
-    mf = t["h"][:n].float().cpu() > 0
+    mf = t["core"][:n, :512].float().cpu() > 0
     return m1, m2, m3, mf
 
 
@@ -83,7 +83,7 @@ def _gpu_grads(net, batch, dl, db):
     net._backward_kernels(dl.cuda(), db.cuda(), cb["reward"].reshape(n), cb["last_action"].reshape(n),
                           grads)
     torch.cuda.synchronize()
-    return dict(zip([k for k, _ in net.named_parameters()], net._split(grads)))
+    return net.torch_layout_grads(grads)
 
 
 @pytest.mark.parametrize("T,B,A", [(2, 3, 6), (7, 16, 18), (80, 32, 6)])

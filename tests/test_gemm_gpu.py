@@ -19,7 +19,7 @@ def _run(M, N, K, a_mn, b_mn, splits=1, seed=0):
     m_pad = ((M + 127) // 128) * 128
     C = torch.full((splits, m_pad, N), float("nan"), device="cuda")
     Nt.check(Nt.lib().bp_gemm_bf16_test(a_store.data_ptr(), b_store.data_ptr(), C.data_ptr(), M, N, K,
-                                        int(a_mn), int(b_mn), splits, Nt.stream_handle()),
+                                        int(a_mn), int(b_mn), splits, 0, Nt.stream_handle()),
              "bp_gemm_bf16_test")
     torch.cuda.synchronize()
     got = C.sum(0)[:M]
@@ -39,6 +39,7 @@ def _run(M, N, K, a_mn, b_mn, splits=1, seed=0):
     (512, 64, 1024, 1, 1, 3),
     (640, 512, 640, 1, 1, 2),
     (256, 64, 512, 0, 1, 1),
+    (384, 128, 576, 0, 1, 1),
     (256, 64, 512, 1, 0, 1),
 ])
 def test_engine_matches_torch(M, N, K, a_mn, b_mn, splits):

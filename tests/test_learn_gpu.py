@@ -46,7 +46,7 @@ def test_learn_step_matches_upstream_restatement(T, B, A):
             assert abs(stats["total_loss"] - total_ref) <= 1e-2 * max(1.0, abs(total_ref))
             assert abs(stats["baseline_loss"] - parts_ref[1]) <= 1e-2 * abs(parts_ref[1])
         assert float(opt.norm) == pytest.approx(norm_ref, rel=5e-2)
-    got = dict(net.named_parameters())
+    got = net.state_dict()  # upstream torch layout
     for k, v in ref.named_parameters():
         upd_ref = (v.detach() - p0[k]).double().reshape(1, -1)
         upd = (got[k].detach().cpu() - p0[k]).double().reshape(1, -1)

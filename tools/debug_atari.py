@@ -58,7 +58,7 @@ a2_g = t["x2"][: n * 81].float().cpu().view(n, 9, 9, 64).permute(0, 3, 1, 2)
 print("a2", rel(a2_g, a2))
 a3_g = t["x3"][:n].float().cpu().view(n, 7, 7, 64).permute(0, 3, 1, 2)
 print("a3", rel(a3_g, a3))
-print("h", rel(t["h"][:n].float().cpu(), h))
+print("h", rel(t["core"][:n, :512].float().cpu(), h))
 print("d_fc", rel(t["d_fc"][:n].float().cpu(), zf.grad))
 d3 = t["d_pre3"][: n * 81].float().cpu().view(n, 9, 9, 64)
 print("d_pre3", rel(d3[:, :7, :7].permute(0, 3, 1, 2), z3.grad),
@@ -69,5 +69,6 @@ print("d_pre2", rel(d2[:, :9, :9].permute(0, 3, 1, 2), z2.grad),
 d1 = t["d_pre1"][: n * 441].float().cpu().view(n, 21, 21, 32)
 print("d_pre1", rel(d1[:, :20, :20].permute(0, 3, 1, 2), z1.grad),
       "pad max", float(d1[:, 20:].abs().max()), float(d1[:, :, 20:].abs().max()))
-for (k, p), v in zip(ref.named_parameters(), net._split(grads)):
-    print(k, rel(v, p.grad))
+tg = net.torch_layout_grads(grads)
+for k, p in ref.named_parameters():
+    print(k, rel(tg[k], p.grad))

@@ -1,0 +1,5 @@
+python -m paper_1910_03552_b200.build > /dev/null 2>&1 || exit 1
+timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -4 gpurun_out/pytest_gpu.log
+timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -3 gpurun_out/bench.log
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:bp:: -s 44 -c 22 --csv --log-file gpurun_out/launches_step.csv python tools/prof_step.py 3 > /dev/null 2>&1; echo "ncu rc=$?"
+python tools/parse_launches.py gpurun_out/launches_step.csv
