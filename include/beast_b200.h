@@ -200,6 +200,13 @@ int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const
  * logits [n][A] f32 -> actions [n] int64. */
 int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
                           int64_t* actions, void* stream);
+/* Shifted-tap GEMM test entry (the convolution form of the engine):
+ * C[m][n] = sum_t sum_c A[m + offs[t]][c] * B[n][t*Cin + c]; window_mode 0 = one TMA box
+ * per tap, 1 / 2 = one shared window per channel block (descriptor base offset 0 / row&7).
+ * trace (nullable, device u64 [grid][trace_tiles][8]): per-tile %globaltimer events
+ * (producer start/end, MMA start/end, epilogue start/end). */
+int bp_gemm_shift_test(const void* A, const void* B, float* C, int R, int Cin, int N, int taps,
+                       const int* offs, int window_mode, void* trace, int trace_tiles, void* stream);
 /* Raw tcgen05 GEMM engine (test entry): C[M][N] = A . B^T, bf16 operands
  * (a_mn / b_mn select MN-major storage), f32 output (bf16 if out_bf16), split-K
  * partials at C + s*M*N. */

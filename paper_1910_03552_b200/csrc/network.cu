@@ -97,6 +97,18 @@ static int make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long 
   return BP_OK;
 }
 
+// window mode for a shifted K-major A operand: taps share one TMA box per channel block
+static void set_window(GemmArgs& g, int taps) {
+  int mn = 0, mx = 0;
+  for (int t = 0; t < taps; ++t) {
+    mn = g.a_row_off[t] < mn ? g.a_row_off[t] : mn;
+    mx = g.a_row_off[t] > mx ? g.a_row_off[t] : mx;
+  }
+  g.a_ntaps = taps;
+  g.a_min_off = mn;
+  g.a_win_rows = (128 + mx - mn + 7) & ~7;
+}
+
 static GemmArgs base_args() {
   GemmArgs g;
   memset(&g, 0, sizeof(g));
@@ -112,10 +124,18 @@ static GemmArgs base_args() {
   return g;
 }
 
-template <int BN, int AM, int BM, int BSWZ>
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0>
 static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, AM, BM, BSWZ>;
-  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ>;
+  using Cfg = GemmCfg<BN, AM, BM, BSWZ, BRES, AW>;
+  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW>;
+  if (AW && (g.a_win_rows > 160 || g.a_win_rows < 128 || g.a_ntaps < 1 || g.a_ntaps > kMaxShifts)) {
+    set_error("gemm: window rows %d / taps %d unsupported", g.a_win_rows, g.a_ntaps);
+    return BP_ERR_ARG;
+  }
+  if (BRES && (g.n_tiles != 1 || g.splits != 1 || (size_t)g.num_kb * Cfg::B_BYTES > Cfg::B_RES)) {
+    set_error("gemm: B-resident mode needs n_tiles == splits == 1 and B <= %u bytes", Cfg::B_RES);
+    return BP_ERR_ARG;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -130,8 +150,6 @@ static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorM
   kern<<<grid, kGemmThreads, Cfg::SMEM, s>>>(g, ta, tb);
   return check_launch("umma_gemm_kernel");
 }
-
-
 
 // ============================================================ support kernels
 
@@ -435,6 +453,53 @@ extern "C" int bp_gemm_bf16_test(const void* A, const void* B, void* C, int M, i
   return BP_ERR_UNSUPPORTED;
 }
 
+// Shifted-tap GEMM test entry: C[m][n] = sum_t sum_c A[m + off_t][c] B[n][t*C + c], A [R][C] K-major,
+// B [N][taps*C]; window_mode 0 = one TMA box per tap, 1/2 = one window per channel block
+// (descriptor base_offset 0 / (addr >> 7) & 7).  N in {32, 64}; C multiple of 64.
+extern "C" int bp_gemm_shift_test(const void* A, const void* B, float* Cout, int R, int Cin, int N,
+                                  int taps, const int* offs, int window_mode, void* trace,
+                                  int trace_tiles, void* stream) {
+  if (int e = init_driver()) return e;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (Cin % 64 || taps < 1 || taps > kMaxShifts || !(N == 32 || N == 64)) {
+    set_error("shift_test: bad args");
+    return BP_ERR_ARG;
+  }
+  int mn = 0, mx = 0;
+  for (int t = 0; t < taps; ++t) {
+    mn = offs[t] < mn ? offs[t] : mn;
+    mx = offs[t] > mx ? offs[t] : mx;
+  }
+  GemmArgs g = base_args();
+  g.m_tiles = (R + 127) / 128;
+  g.n_tiles = 1;
+  g.a_cb = Cin / 64;
+  g.num_kb = g.kb_per_split = taps * g.a_cb;
+  for (int t = 0; t < taps; ++t) g.a_row_off[t] = offs[t];
+  g.a_ntaps = taps;
+  g.a_min_off = mn;
+  g.a_win_rows = (128 + mx - mn + 7) & ~7;
+  g.N = N;
+  g.M = R;
+  g.out_f32 = 1;
+  g.out = Cout;
+  g.r_img = N;
+  g.trace = reinterpret_cast<unsigned long long*>(trace);
+  g.trace_tiles = trace_tiles;
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap(&ta, A, R, Cin, 64, window_mode ? g.a_win_rows : 128, 128))) return rc;
+  if ((rc = make_tmap(&tb, B, N, (long long)taps * Cin, 64, N, 128))) return rc;
+  if (N == 32) {
+    if (window_mode == 0) return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 0>(g, ta, tb, s);
+    if (window_mode == 1) return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s);
+    return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 2>(g, ta, tb, s);
+  }
+  if (window_mode == 0) return launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 0>(g, ta, tb, s);
+  if (window_mode == 1) return launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s);
+  return launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 2>(g, ta, tb, s);
+}
+
 extern "C" int64_t bp_atari_param_count(int num_actions, int use_lstm) {
   if (num_actions < 1 || num_actions > 31 || use_lstm) return -1;
   int64_t off[P_COUNT + 1];
@@ -497,14 +562,15 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
   // 2. conv1: X0 [n*441, 64] x W1 [32, 256] -> relu(./255 + b1) -> X1 (s2d-2 layout)
   {
     const long long R = (long long)n * 441;
-    if ((rc = make_tmap(&ta, net->x0, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_W1], 32, 256, 64, 32, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 4;
     const int offs[4] = {0, 1, 21, 22};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = offs[i];
+    set_window(g, 4);
+    if ((rc = make_tmap(&ta, net->x0, R, 64, 64, g.a_win_rows, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W1], 32, 256, 64, 32, 128))) return rc;
     g.N = 32;
     g.M = (int)R;
     g.alpha = 1.f / 255.f;
@@ -514,13 +580,11 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bits_out = reinterpret_cast<uint32_t*>(net->m1);
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
-    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // 3. conv2: X1 [n*100, 128], 2x2 taps on the 10x10 grid -> X2 [n*81, 64]
   {
     const long long R = (long long)n * 100;
-    if ((rc = make_tmap(&ta, net->x1, R, 128, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
@@ -528,6 +592,9 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.a_cb = 2;
     const int offs[4] = {0, 1, 10, 11};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = offs[i];
+    set_window(g, 4);
+    if ((rc = make_tmap(&ta, net->x1, R, 128, 64, g.a_win_rows, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     g.N = 64;
     g.M = (int)R;
     g.bias = params + off[P_B2];
@@ -536,19 +603,20 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bits_out = reinterpret_cast<uint32_t*>(net->m2);
     g.gh = 10; g.gw = 10; g.vh = 9; g.vw = 9;
     g.r_img = 81 * 64; g.r_y = 9 * 64; g.r_x = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // 4. conv3: X2 [n*81, 64], 3x3 taps on the 9x9 grid -> X3 [n, 3136] ((y, x, c) order)
   {
     const long long R = (long long)n * 81;
-    if ((rc = make_tmap(&ta, net->x2, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 9;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) g.a_row_off[dy * 3 + dx] = dy * 9 + dx;
+    set_window(g, 9);
+    if ((rc = make_tmap(&ta, net->x2, R, 64, 64, g.a_win_rows, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     g.N = 64;
     g.M = (int)R;
     g.bias = params + off[P_B3];
@@ -557,7 +625,7 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.bits_out = reinterpret_cast<uint32_t*>(net->m3);
     g.gh = 9; g.gw = 9; g.vh = 7; g.vw = 7;
     g.r_img = 3136; g.r_y = 7 * 64; g.r_x = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // 5. fc: X3 [n, 3136] x Wfc [512, 3136] -> core[:, :512] = relu(. + bfc)
   {
@@ -592,7 +660,7 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.A = A;
     g.logits = logits;
     g.baseline = baseline;
-    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s))) return rc;
   }
   return BP_OK;
 }
@@ -659,14 +727,15 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
   // 4. conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
   {
     const long long R = (long long)n * 81;
-    if ((rc = make_tmap(&ta, net->d_pre3, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 9;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) g.a_row_off[dy * 3 + dx] = -(dy * 9 + dx);
+    set_window(g, 9);
+    if ((rc = make_tmap(&ta, net->d_pre3, R, 64, 64, g.a_win_rows, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W3], 64, 576, 64, 64, 128))) return rc;
     g.b_kb_per_tap = 1;
     g.b_tap_stride = 64;
     g.N = 64;
@@ -676,19 +745,20 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.gh = 9; g.gw = 9; g.vh = 9; g.vw = 9;
     g.r_img = 100 * 64; g.r_y = 10 * 64; g.r_x = 64;
     g.colsum = ws + P.cs_off[1];
-    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // 5. conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
   {
     const long long R = (long long)n * 100;
-    if ((rc = make_tmap(&ta, net->d_pre2, R, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
     g.m_tiles = (int)((R + 127) / 128);
     g.n_tiles = 1;
     g.num_kb = g.kb_per_split = 4;
     const int offs[4] = {0, 1, 10, 11};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = -offs[i];
+    set_window(g, 4);
+    if ((rc = make_tmap(&ta, net->d_pre2, R, 64, 64, g.a_win_rows, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_W2], 64, 512, 64, 64, 128))) return rc;
     g.b_kb_per_tap = 1;
     g.b_tap_stride = 128;
     g.N = 128;
@@ -699,7 +769,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.r_img = 441 * 32; g.r_y = 2 * 21 * 32; g.r_x = 2 * 32;
     g.cdiv = 32; g.cq = 2; g.cs1 = 21 * 32; g.cs2 = 32;
     g.colsum = ws + P.cs_off[0];
-    if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // 6. weight gradients
   auto wgrad = [&](int i, const void* X, long long xrows, int xcols, int atoms_per_shift, int nshifts,
