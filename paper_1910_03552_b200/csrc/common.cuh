@@ -47,6 +47,9 @@ BP_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+BP_DEVICE void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 BP_DEVICE void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nW_%=:\n"
@@ -83,8 +86,21 @@ BP_DEVICE void st_cs4(float4* p, float4 v) {
 // math: fast exp/log with ~1 ulp-class error (MUFU ex2/lg2), fine for the
 // 1e-5 relative V-trace tolerance.
 // ---------------------------------------------------------------------------
-BP_DEVICE float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
-BP_DEVICE float fast_log(float x) { return __logf(x); }
+BP_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+BP_DEVICE float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+BP_DEVICE float fast_exp(float x) { return ex2_approx(x * 1.4426950408889634f); }
+BP_DEVICE float fast_log(float x) { return lg2_approx(x) * 0.6931471805599453f; }
+BP_DEVICE void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
 
 template <typename T>
 BP_DEVICE T warp_sum(T v) {

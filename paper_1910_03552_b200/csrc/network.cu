@@ -32,6 +32,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tma_host.h"
 #include "umma_gemm.cuh"
 
 namespace bp {
@@ -53,48 +54,14 @@ static void param_offsets(int A, int64_t* off) {
   off[P_COUNT] = o;
 }
 
-// ============================================================ tensor maps
-static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-static int g_num_sms = 0;
-
-static int init_driver() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  if (!g_encode) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return BP_ERR_LAUNCH;
-  }
-  return BP_OK;
-}
+// ============================================================ tensor maps (tma_host.cu)
+static int init_driver() { return tma_init(); }
+#define g_num_sms tma_num_sms()
 
 // bf16 row-major [rows][cols]; box {box_cols (inner), box_rows}
 static int make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, int box_cols,
                      int box_rows, int swz) {
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapSwizzle sw = swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld box=%dx%d", (int)r, rows, cols,
-              box_cols, box_rows);
-    return BP_ERR_LAUNCH;
-  }
-  return BP_OK;
+  return tma_make_2d(m, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, box_cols, box_rows, swz);
 }
 
 // window mode for a shifted K-major A operand: taps share one TMA box per channel block
