@@ -184,10 +184,29 @@ __global__ void __launch_bounds__(kThreads) vt2_kernel(const __grid_constant__ A
         if constexpr (!LOSS) sm100::tma_load_2d(in + P.in_disc, &mp.disc, &sfull[set], b0, 0);
       }
       if constexpr (LOSS) {  // discount = (float)gamma * ~done, exact
-        float* s_disc = reinterpret_cast<float*>(in + P.in_disc);
-        for (int i = lane; i < T * BT; i += 32) {
-          const int t = i / BT, b = i % BT;
-          s_disc[i] = (b0 + b < B && g.done[(size_t)t * B + b0 + b]) ? 0.f : g.discount;
+        float4* s_disc4 = reinterpret_cast<float4*>(in + P.in_disc);
+        const float gm = g.discount;
+        if ((B & 3) == 0 && b0 + 4 <= B) {
+          // the 4 flags of a time row are one aligned u32: issue all loads, then convert
+          uint32_t w[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int t = lane + 32 * k;
+            w[k] = t < T ? __ldg(reinterpret_cast<const uint32_t*>(g.done + (size_t)t * B + b0)) : 0u;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int t = lane + 32 * k;
+            if (t < T)
+              s_disc4[t] = make_float4((w[k] & 0xffu) ? 0.f : gm, (w[k] & 0xff00u) ? 0.f : gm,
+                                       (w[k] & 0xff0000u) ? 0.f : gm, (w[k] & 0xff000000u) ? 0.f : gm);
+          }
+        } else {
+          float* s_disc = reinterpret_cast<float*>(s_disc4);
+          for (int i = lane; i < T * BT; i += 32) {
+            const int t = i / BT, b = i % BT;
+            s_disc[i] = (b0 + b < B && g.done[(size_t)t * B + b0 + b]) ? 0.f : gm;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&sfull[set]);
@@ -371,6 +390,7 @@ __global__ void __launch_bounds__(kThreads) vt2_kernel(const __grid_constant__ A
       if (tid < bw) g.d_baseline[(size_t)T * B + b0 + tid] = 0.f;
       cons_sync();
       // ---------------------------------------------------------- phase 3: d_logits
+      int pending = -1;  // stage whose TMA store may still be reading smem (released one chunk later)
       for (int c = 0; c < nchunks; ++c, ++q) {
         const int s = q % kNst;
         mbar_wait_parity(&full[s], (q / kNst) & 1u);
@@ -393,9 +413,16 @@ __global__ void __launch_bounds__(kThreads) vt2_kernel(const __grid_constant__ A
         if (tid == 0) {
           tma_store_2d(&mp.dlog, stg, b0 * A, c * TC);  // clipped at the tensor edges
           bulk_commit();
-          bulk_wait_read_all();
-          mbar_arrive_cnt(&empty[s], kCons / 32);
+          if (pending >= 0) {
+            bulk_wait_read_1();  // every store but the newest has read its stage
+            mbar_arrive_cnt(&empty[pending], kCons / 32);
+          }
+          pending = s;
         }
+      }
+      if (tid == 0 && pending >= 0) {
+        bulk_wait_read_all();
+        mbar_arrive_cnt(&empty[pending], kCons / 32);
       }
     }
     cons_sync();
