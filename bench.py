@@ -345,6 +345,27 @@ def main():
                "frac": vt["gbs"] / pk["hbm"], "traffic": None, "bytes": vt["bytes"],
                "seconds": vt["median_s"]}
     ll = kernel_bench.bench_loss(T, B, A, timer, iters=20)
+    vt_sweep = {}
+    for bb in (4096, 16384, 65536):
+        r = kernel_bench.bench_vtrace(80, bb, 18, timer, iters=10)
+        rl = kernel_bench.bench_loss(80, bb, 18, timer, iters=10)
+        vt_sweep[str(bb)] = {"vtrace_gbs": r["gbs"], "vtrace_frac": r["gbs"] / pk["hbm"],
+                             "loss_gbs": rl["gbs"], "loss_frac": rl["gbs"] / pk["hbm"]}
+    # configs[4]: actor-inference forward (PolyBeast dynamic batching) on 1024 observations,
+    # forward + Gumbel-max action sampling, CUDA-graphed
+    inf = None
+    if rank == 0:
+        ib = make_batch(0, 1024, A, dev, seed=9)
+        inputs = {k: ib[k] for k in ("frame", "reward", "done", "last_action")}
+        model.eval()
+        with torch.no_grad():
+            fwd = lambda: model(inputs)  # noqa: E731
+            ri = timer.time(fwd, iters=20, warmup=3, flush=True, graph=True)
+        model.train()
+        inf_flops = 2 * 1024 * sum(MACS.values())
+        inf = {"workload": "configs[4]: AtariNet forward + sampling, 1024 obs 4x84x84",
+               "ms": ri["median_s"] * 1e3, "obs_per_s": 1024 / ri["median_s"],
+               "tflops": inf_flops / ri["median_s"] / 1e12}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -363,7 +384,8 @@ def main():
                            "read back each step; one CUDA-event window over all steps"},
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
             "roofline": roofline, "vtrace_roofline": vt_roof,
-            "learner_loss_kernel_s": ll["median_s"],
+            "learner_loss_kernel_s": ll["median_s"], "vtrace_sweep": vt_sweep,
+            "inference": inf,
             "cpu_baseline": cpu, "clocks": clk.summary(),
             "stats_last": {k: stats[k] for k in ("total_loss", "pg_loss", "baseline_loss",
                                                  "entropy_loss")},

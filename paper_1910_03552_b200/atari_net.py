@@ -97,7 +97,7 @@ class _Buffers:
 class _AtariFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, net, frames, reward, last_action, *params):
-        logits, baseline = net._forward_kernels(frames, reward, last_action)
+        logits, baseline = net._forward_kernels(frames, reward, last_action, repack=True)
         ctx.net = net
         ctx.save_for_backward(reward, last_action)
         return logits, baseline
@@ -210,15 +210,23 @@ class AtariNet(nn.Module):
                                               N.stream_handle(self.flat_params.device)),
                 "bp_atari_pack_weights")
         self.mirror_fresh = True
+        self._packed_version = self.flat_params._version
+
+    def mirror_stale(self) -> bool:
+        """True if the bf16 mirror may lag the f32 parameters: never packed, or the
+        parameters were modified in place through torch since (version counter)."""
+        return (not self.mirror_fresh or
+                getattr(self, "_packed_version", None) != self.flat_params._version)
 
     def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
-                         repack: bool = True):
+                         repack: bool | None = None):
         """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
 
-        repack=False trusts the bf16 mirror (kept fresh by the fused optimiser step)."""
+        repack=None packs the bf16 mirror only when stale; False trusts it (the fused
+        optimiser step keeps it fresh); True always packs."""
         n = frames.shape[0]
         b = self.buffers_for(n)
-        if repack or not self.mirror_fresh:
+        if repack or (repack is None and self.mirror_stale()):
             self.pack_weights()
         if logits is None:
             logits = torch.empty(n, self.num_actions, device=frames.device)

@@ -64,6 +64,11 @@ class FusedLearner:
         self._graphs: dict = {}
         self._seen: set = set()
 
+    def _pg_is_nccl(self) -> bool:
+        """NCCL collectives can be captured in a CUDA graph; gloo ones cannot."""
+        grp = None if self.pg is True else self.pg
+        return torch.distributed.get_backend(grp) == "nccl"
+
     def _graph_key(self, batch, optimizer):
         keys = ("frame", "reward", "done", "policy_logits", "action", "last_action")
         return tuple(batch[k].data_ptr() for k in keys) + (id(optimizer),)
@@ -77,7 +82,7 @@ class FusedLearner:
         replayed, so host launch overhead leaves the critical path.  The first
         call per buffer set runs eagerly (warm-up), the second captures.
         """
-        graphable = (self.use_graphs and self.pg is None and
+        graphable = (self.use_graphs and (self.pg is None or self._pg_is_nccl()) and
                      (optimizer is None or (isinstance(optimizer, RMSprop) and
                                             optimizer.flat_params.data_ptr() ==
                                             self.model.flat_params.data_ptr())))
@@ -86,6 +91,8 @@ class FusedLearner:
             g = self._graphs.get(key)
             if g is None and key in self._seen:
                 optimizer and optimizer.sync_lr()
+                if self.model.mirror_stale():  # the captured step must not contain the pack
+                    self.model.pack_weights()
                 g = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
@@ -98,6 +105,8 @@ class FusedLearner:
             if g is not None:
                 if optimizer is not None:
                     optimizer.sync_lr()
+                if self.model.mirror_stale():  # e.g. load_state_dict between steps
+                    self.model.pack_weights()
                 g.replay()
                 if scheduler is not None:
                     scheduler.step()
@@ -119,7 +128,7 @@ class FusedLearner:
         # 1. forward (the bf16 operand mirror is refreshed by the fused optimiser below)
         m._forward_kernels(frames.reshape(n, *m.observation_shape), reward.reshape(n),
                            last_action.reshape(n), logits=self.logits, baseline=self.baseline,
-                           repack=False)
+                           repack=None)  # packs only if stale (first step, load_state_dict, ...)
         # 2. fused V-trace + losses + gradients w.r.t. logits / baseline
         self.loss(self.logits[:T * B].view(T, B, A), self.baseline.view(T + 1, B),
                   batch["policy_logits"][1:], batch["action"][1:], reward[1:], batch["done"][1:],
@@ -128,15 +137,19 @@ class FusedLearner:
         # 3. backward into the flat gradient buffer
         m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
                             m.flat_grads)
-        # 4. data-parallel: sum gradients over ranks (losses are sums over T x B)
+        # 4. data-parallel over B: the losses are sums over (T, B) (vtrace.py:194-196), so
+        #    the full-batch gradient is the SUM of the shard gradients (one all-reduce of the
+        #    flat f32 buffer); the loss scalars are summed too, for the stats
         if self.pg is not None:
-            torch.distributed.all_reduce(m.flat_grads, op=torch.distributed.ReduceOp.SUM,
-                                         group=self.pg if self.pg is not True else None)
+            grp = self.pg if self.pg is not True else None
+            torch.distributed.all_reduce(m.flat_grads, op=torch.distributed.ReduceOp.SUM, group=grp)
+            torch.distributed.all_reduce(self.losses, op=torch.distributed.ReduceOp.SUM, group=grp)
         # 5. clip + RMSProp
         if optimizer is not None:
             if isinstance(optimizer, RMSprop) and optimizer.flat_params.data_ptr() == m.flat_params.data_ptr():
                 optimizer.step(max_norm=self.max_norm, mirror=m.flat_bf16)  # params + bf16 mirror
                 m.mirror_fresh = True
+                m._packed_version = m.flat_params._version
             else:  # any torch optimiser: device-side norm + clip, then its own step
                 ss = torch.zeros(1, dtype=torch.float64, device=m.flat_grads.device)
                 sumsq_(m.flat_grads, ss)

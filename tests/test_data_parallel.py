@@ -1,0 +1,67 @@
+"""Data parallelism over B: shard gradients SUM-reduce to the full-batch gradient.
+
+CPU: the torch oracle on 2 gloo ranks.  GPU: the fused learner's all-reduce path on 2
+gloo ranks sharing one device (the NCCL path differs only in the backend name)."""
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+import dp_worker
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = q.get(timeout=240)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    return res
+
+
+def test_shard_gradient_sum_equals_full_batch_oracle():
+    rel, tot, full = _run(dp_worker.oracle_dp)
+    assert rel < 1e-5
+    assert abs(tot - full) <= 1e-4 * max(1.0, abs(full))
+
+
+def test_training_batch_shard_columns():
+    import torch
+
+    from paper_1910_03552_b200.rollout import TrainingBatch
+
+    t1, b = 5, 8
+    tb = TrainingBatch(observation=torch.arange(t1 * b).reshape(t1, b), reward=torch.zeros(t1, b),
+                       done=torch.zeros(t1, b, dtype=torch.bool), policy_logits=torch.zeros(t1, b, 3),
+                       baseline=torch.zeros(t1, b), action=torch.zeros(t1, b, dtype=torch.int64),
+                       model_versions=torch.arange(b))
+    parts = [tb.shard(r, 4) for r in range(4)]
+    assert all(p.batch_size == 2 for p in parts)
+    assert torch.equal(torch.cat([p.observation for p in parts], 1), tb.observation)
+    assert torch.equal(torch.cat([p.model_versions for p in parts]), tb.model_versions)
+
+
+@pytest.mark.gpu
+def test_fused_learner_data_parallel_matches_single_process():
+    same, cos, losses, losses1 = _run(dp_worker.fused_dp)
+    assert same, "every rank must apply the identical update"
+    assert cos > 0.999, cos
+    for a, b in zip(losses, losses1):
+        assert abs(a - b) <= 1e-3 * max(1.0, abs(b))

@@ -70,3 +70,23 @@ def test_learn_is_repeatable_and_finite():
         assert all(map(lambda x: x == x, [stats["total_loss"], stats["pg_loss"]]))
         outs.append(net.flat_params.clone())
     assert torch.equal(outs[0], outs[1]), "fused learner step must be deterministic"
+
+
+def test_learn_after_load_state_dict_uses_new_weights():
+    """The bf16 operand mirror must follow load_state_dict, also on graph replays."""
+    from paper_1910_03552_b200 import learner, optim
+    from paper_1910_03552_b200.atari_net import AtariNet
+
+    flags = dict(atari_ref.DEFAULT_FLAGS)
+    torch.manual_seed(2)
+    net = AtariNet(num_actions=6)
+    opt = optim.RMSprop(net.parameters(), lr=flags["learning_rate"], alpha=0.99, eps=0.01)
+    batch = {k: v.cuda() for k, v in atari_ref.synthetic_batch(4, 4, 6, seed=1).items()}
+    for _ in range(3):  # eager, capture, replay
+        learner.learn(flags, None, net, batch, (), opt, None)
+    ref = atari_ref.AtariNetRef(num_actions=6)
+    net.load_state_dict(ref.state_dict())
+    ropt = torch.optim.RMSprop(ref.parameters(), lr=flags["learning_rate"], alpha=0.99, eps=0.01)
+    total_ref, _, _ = atari_ref.learn_step(ref, ropt, {k: v.cpu() for k, v in batch.items()}, flags)
+    stats = learner.learn(flags, None, net, batch, (), opt, None)  # graph replay path
+    assert abs(stats["total_loss"] - total_ref) <= 1e-2 * max(1.0, abs(total_ref))
