@@ -146,6 +146,7 @@ int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t 
 typedef struct BpAtariNet {
   int num_actions; /* A in [1, 31] */
   int max_frames;  /* capacity N */
+  int use_lstm;    /* 1: parameter layout with the LSTM core (bp_atari_lstm_*) */
   void* wbf;  /* bf16 mirror of the flat f32 parameters (GEMM operands) */
   void* whf;  /* [32][576] bf16 heads operand: [Wp | bp], [Wv | bv], zero rows */
   /* activations, bf16 */
@@ -171,16 +172,20 @@ typedef struct BpAtariNet {
 } BpAtariNet;
 
 /* f32 master parameter layout (flat, upstream AtariNet module order):
- * conv1.weight, conv1.bias, conv2.weight, conv2.bias, conv3.weight, conv3.bias,
- * fc.weight, fc.bias, policy.weight [A][513+A], policy.bias,
- * baseline.weight [1][513+A], baseline.bias; offsets[12] = total count.
+ * [0] conv1.weight, [1] conv1.bias, [2] conv2.weight, [3] conv2.bias, [4] conv3.weight,
+ * [5] conv3.bias, [6] fc.weight, [7] fc.bias,
+ * [8..15] (use_lstm only, else empty) core.weight_ih_l0 [4H][H], core.weight_hh_l0 [4H][H],
+ *         core.bias_ih_l0 [4H], core.bias_hh_l0 [4H], the same four for layer 1 (H = 513+A,
+ *         torch nn.LSTM layout and gate order i, f, g, o),
+ * [16] policy.weight [A][513+A], [17] policy.bias, [18] baseline.weight [1][513+A],
+ * [19] baseline.bias; offsets[20] = total count.
  * Conv / fc weights are stored in GEMM layout [Cout][K], K = (tap, channel):
  *   conv1 k = (dy*2+dx)*64 + ci*16 + ry*4 + rx   (ky = 4dy+ry, kx = 4dx+rx)
  *   conv2 k = (dy*2+dx)*128 + (py*2+px)*32 + c    (ky = 2dy+py, kx = 2dx+px)
  *   conv3 k = (dy*3+dx)*64 + c;   fc k = (y*7+x)*64 + c
  * (the Python module converts to / from the torch layouts in state_dicts). */
 int64_t bp_atari_param_count(int num_actions, int use_lstm);
-int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* offsets /* 13 */);
+int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* offsets /* 21 */);
 size_t bp_atari_workspace_bytes(int num_actions, int max_frames);
 /* bf16 mirror of the f32 master parameters (needed after parameters change outside
  * bp_rmsprop_clip_f32 with a mirror output, e.g. after load / init) */
@@ -194,6 +199,47 @@ int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const 
  * same layout as params; every entry is overwritten). */
 int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
                       const float* reward, const int64_t* last_action, float* grads, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * LSTM core (AtariNet(use_lstm=True): upstream nn.LSTM(H, H, 2), H = 513 + A,
+ * stepped per time row with the done reset core_state = notdone_t * core_state).
+ * Input projections and weight / input gradients are tcgen05 GEMMs over all
+ * N = T1*B rows; the recurrence runs as persistent cooperative kernels (one grid
+ * barrier per step, W_hh resident in shared memory, f32 recurrent arithmetic).
+ * G4 = 4H rounded up to a multiple of 128.  Buffers marked "zeroed once" must be
+ * zero at allocation (padding columns are never written).
+ * ------------------------------------------------------------------------- */
+typedef struct BpLstmCore {
+  int hidden;     /* H = 513 + A */
+  int max_rows;   /* capacity N = T1 * B */
+  void* wih;      /* [2][G4][576] bf16 [W_ih | b_ih + b_hh | 0], rows >= 4H zero   */
+  float* gx;      /* [N][G4] input projection of the current layer            */
+  float* gates;   /* [2][N][4H] activated gates i, f, g, o                   */
+  float* cseq;    /* [2][N][H] cell states                                   */
+  void* hprev;    /* [2][N][576] bf16 [notdone_t h_{t-1} | 1 | 0], zeroed once */
+  void* out;      /* [2][N][576] bf16 [h_t | 1 | 0], zeroed once; out[1] feeds the heads */
+  float* hx;      /* [2][H][32] recurrent exchange                           */
+  float* part;    /* bp_lstm_partial_floats(H) backward exchange             */
+  void* dgates;   /* [N][G4] bf16 pre-activation gate gradients, zeroed once */
+  float* dh;      /* [N][576] f32                                            */
+  float* dx;      /* [N][576] f32                                            */
+  float* wpart;   /* [2][G4][576] f32 weight-gradient GEMM outputs           */
+} BpLstmCore;
+size_t bp_lstm_partial_floats(int hidden);
+/* Forward of T1*B frames through torso + LSTM core + heads.  done [T1*B] u8;
+ * h0, c0 [2][B][H] f32 initial state (layer-major, torch (num_layers, B, H));
+ * hN, cN [2][B][H] receive the final state.  B is split into recurrent passes of <= 32. */
+int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                          const uint8_t* frames, const float* reward, const int64_t* last_action,
+                          const uint8_t* done, const float* params, const float* h0, const float* c0,
+                          float* logits, float* baseline, float* hN, float* cN, void* stream);
+/* Backward of the last bp_atari_lstm_forward (same T1, B, done, c0): d_logits [N][A],
+ * d_baseline [N] -> grads (flat, every entry overwritten).  The initial state gets no
+ * gradient (upstream learn() feeds the actors' state as a constant). */
+int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                           const float* d_logits, const float* d_baseline, const uint8_t* done,
+                           const float* params, const float* c0, float* grads, void* stream);
+
 /* Categorical sampling per row (Gumbel-max, counter-based hash RNG keyed by
  * (seed, row, column)); greedy != 0 -> argmax.  Replaces sample_actions
  * (model.py:218-221) / upstream torch.multinomial(softmax(logits)).

@@ -42,6 +42,9 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_pack_weights": (I, [P, P, P]),
     "bp_atari_forward": (I, [P, I, P, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
+    "bp_lstm_partial_floats": (SZ, [I]),
+    "bp_atari_lstm_forward": (I, [P, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),
     "bp_gemm_shift_test": (I, [P, P, P, I, I, I, I, P, I, P, I, P]),
@@ -51,11 +54,20 @@ SIGNATURES: dict[str, tuple] = {
 class BpAtariNet(C.Structure):
     """Mirror of `BpAtariNet` in include/beast_b200.h (field order matters)."""
 
-    _fields_ = [("num_actions", C.c_int), ("max_frames", C.c_int)] + [
+    _fields_ = [("num_actions", C.c_int), ("max_frames", C.c_int), ("use_lstm", C.c_int)] + [
         (name, C.c_void_p) for name in (
             "wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
             "d_pre3", "d_pre2", "d_pre1", "ws")
     ] + [("ws_bytes", C.c_size_t)]
+
+
+class BpLstmCore(C.Structure):
+    """Mirror of `BpLstmCore` in include/beast_b200.h (field order matters)."""
+
+    _fields_ = [("hidden", C.c_int), ("max_rows", C.c_int)] + [
+        (name, C.c_void_p) for name in (
+            "wih", "gx", "gates", "cseq", "hprev", "out", "hx", "part", "dgates", "dh", "dx", "wpart")
+    ]
 
 
 def load(path: str = LIB_PATH):

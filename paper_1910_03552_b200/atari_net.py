@@ -61,10 +61,38 @@ def gemm_to_torch(name: str, w: torch.Tensor) -> torch.Tensor:
 GEMM_WEIGHTS = ("conv1.weight", "conv2.weight", "conv3.weight", "fc.weight")
 
 
+class _LstmBuffers:
+    """Caller-owned device buffers of the C ABI struct BpLstmCore, for n <= capacity rows."""
+
+    def __init__(self, num_actions: int, capacity: int, device):
+        H = 513 + num_actions
+        G4 = (4 * H + 127) // 128 * 128
+        n, d, bf, f32 = capacity, device, torch.bfloat16, torch.float32
+        self.hidden = H
+        self.t = dict(
+            wih=torch.empty(2, G4, 576, dtype=bf, device=d),
+            gx=torch.empty(n, G4, dtype=f32, device=d),
+            gates=torch.empty(2, n, 4 * H, dtype=f32, device=d),
+            cseq=torch.empty(2, n, H, dtype=f32, device=d),
+            # padding columns of these are never written: zero once
+            hprev=torch.zeros(2, n, 576, dtype=bf, device=d),
+            out=torch.zeros(2, n, 576, dtype=bf, device=d),
+            hx=torch.empty(2, H, 32, dtype=f32, device=d),
+            part=torch.empty(N.lib().bp_lstm_partial_floats(H), dtype=f32, device=d),
+            dgates=torch.zeros(n, G4, dtype=bf, device=d),
+            dh=torch.empty(n, 576, dtype=f32, device=d),
+            dx=torch.empty(n, 576, dtype=f32, device=d),
+            wpart=torch.empty(2, G4, 576, dtype=f32, device=d),
+        )
+        names = ("wih", "gx", "gates", "cseq", "hprev", "out", "hx", "part", "dgates", "dh", "dx", "wpart")
+        self.struct = N.BpLstmCore(H, capacity, *[self.t[k].data_ptr() for k in names])
+        self.ref = C.byref(self.struct)
+
+
 class _Buffers:
     """Caller-owned device buffers of the C ABI struct BpAtariNet, for n <= capacity."""
 
-    def __init__(self, num_actions: int, capacity: int, nparams: int, device):
+    def __init__(self, num_actions: int, capacity: int, nparams: int, device, use_lstm: bool = False):
         self.capacity = capacity
         d = device
         bf = torch.bfloat16
@@ -89,9 +117,10 @@ class _Buffers:
         self.t["ws"] = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=d)
         names = ("wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
                  "d_pre3", "d_pre2", "d_pre1", "ws")
-        self.struct = N.BpAtariNet(num_actions, capacity, *[self.t[k].data_ptr() for k in names],
-                                   ws_bytes)
+        self.struct = N.BpAtariNet(num_actions, capacity, int(use_lstm),
+                                   *[self.t[k].data_ptr() for k in names], ws_bytes)
         self.ref = C.byref(self.struct)
+        self.lstm = _LstmBuffers(num_actions, capacity, device) if use_lstm else None
 
 
 class _AtariFunction(torch.autograd.Function):
@@ -112,13 +141,34 @@ class _AtariFunction(torch.autograd.Function):
         return (None, None, None, None, *views)
 
 
+class _AtariLstmFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, net, frames, reward, last_action, done, h0, c0, T1, B, *params):
+        lstm = dict(T1=T1, B=B, done=done, h0=h0, c0=c0)
+        logits, baseline = net._forward_kernels(frames, reward, last_action, repack=True, lstm=lstm)
+        ctx.net = net
+        ctx.dims = (T1, B)
+        ctx.save_for_backward(reward, last_action, done, c0)
+        ctx.mark_non_differentiable(lstm["hN"], lstm["cN"])
+        return logits, baseline, lstm["hN"], lstm["cN"]
+
+    @staticmethod
+    def backward(ctx, d_logits, d_baseline, d_hN, d_cN):
+        net = ctx.net
+        reward, last_action, done, c0 = ctx.saved_tensors
+        T1, B = ctx.dims
+        grads = torch.empty_like(net.flat_params)
+        net._backward_kernels(d_logits, d_baseline, reward, last_action, grads,
+                              lstm=dict(T1=T1, B=B, done=done, c0=c0))
+        views = net._split(grads)
+        return (None,) * 9 + tuple(views)
+
+
 class AtariNet(nn.Module):
     def __init__(self, observation_shape=OBS_SHAPE, num_actions=6, use_lstm=False, device=None):
         super().__init__()
         if tuple(observation_shape) != OBS_SHAPE:
             raise DimensionError(f"AtariNet kernels take {OBS_SHAPE} u8 frames, got {observation_shape}")
-        if use_lstm:
-            raise NotImplementedError("LSTM core: see DESIGN.md (not in this build yet)")
         if not 1 <= num_actions <= 31:
             raise DimensionError("num_actions must be in [1, 31]")
         self.observation_shape = tuple(observation_shape)
@@ -131,6 +181,8 @@ class AtariNet(nn.Module):
         self.conv3 = nn.Conv2d(64, 64, kernel_size=3, stride=1)
         self.fc = nn.Linear(3136, 512)
         core = self.fc.out_features + num_actions + 1
+        if use_lstm:  # upstream: nn.LSTM(core_output_size, core_output_size, 2)
+            self.core = nn.LSTM(core, core, 2)
         self.policy = nn.Linear(core, num_actions)
         self.baseline = nn.Linear(core, 1)
         self.to(device)
@@ -140,7 +192,7 @@ class AtariNet(nn.Module):
             for name in GEMM_WEIGHTS:
                 mod = getattr(self, name.split(".")[0])
                 mod.weight = nn.Parameter(torch_to_gemm(name, mod.weight.detach()).contiguous())
-        count = N.lib().bp_atari_param_count(num_actions, 0)
+        count = N.lib().bp_atari_param_count(num_actions, int(use_lstm))
         params = list(self.parameters())
         assert sum(p.numel() for p in params) == count
         self.flat_params = torch.empty(count, dtype=torch.float32, device=device)
@@ -192,7 +244,8 @@ class AtariNet(nn.Module):
 
     def buffers_for(self, n: int) -> _Buffers:
         if self._bufs is None or self._bufs.capacity < n:
-            self._bufs = _Buffers(self.num_actions, n, self.flat_params.numel(), self.flat_params.device)
+            self._bufs = _Buffers(self.num_actions, n, self.flat_params.numel(), self.flat_params.device,
+                                  self.use_lstm)
             self._logits = torch.empty(n, self.num_actions, device=self.flat_params.device)
             self._baseline = torch.empty(n, device=self.flat_params.device)
             self.mirror_fresh = False
@@ -219,11 +272,13 @@ class AtariNet(nn.Module):
                 getattr(self, "_packed_version", None) != self.flat_params._version)
 
     def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
-                         repack: bool | None = None):
+                         repack: bool | None = None, lstm: dict | None = None):
         """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
 
         repack=None packs the bf16 mirror only when stale; False trusts it (the fused
-        optimiser step keeps it fresh); True always packs."""
+        optimiser step keeps it fresh); True always packs.  LSTM nets take
+        lstm=dict(T1, B, done u8 (n,), h0, c0 (2,B,H) f32[, hN, cN]); the final state
+        is returned in lstm["hN"], lstm["cN"]."""
         n = frames.shape[0]
         b = self.buffers_for(n)
         if repack or (repack is None and self.mirror_stale()):
@@ -232,20 +287,43 @@ class AtariNet(nn.Module):
             logits = torch.empty(n, self.num_actions, device=frames.device)
         if baseline is None:
             baseline = torch.empty(n, device=frames.device)
-        N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), N.ptr(reward), N.ptr(last_action),
-                                         N.ptr(self.flat_params), N.ptr(logits), N.ptr(baseline),
-                                         N.stream_handle(frames.device)), "bp_atari_forward")
+        stream = N.stream_handle(frames.device)
+        if self.use_lstm:
+            if lstm is None:
+                raise DimensionError("LSTM AtariNet forward needs done / core_state (lstm=...)")
+            T1, B = lstm["T1"], lstm["B"]
+            if T1 * B != n:
+                raise DimensionError(f"lstm dims {T1}x{B} != {n} frames")
+            shape = (2, B, self.core_hidden)
+            for k in ("hN", "cN"):
+                if lstm.get(k) is None:
+                    lstm[k] = torch.empty(shape, device=frames.device)
+            N.check(N.lib().bp_atari_lstm_forward(
+                b.ref, b.lstm.ref, T1, B, N.ptr(frames), N.ptr(reward), N.ptr(last_action),
+                N.ptr(lstm["done"]), N.ptr(self.flat_params), N.ptr(lstm["h0"]), N.ptr(lstm["c0"]),
+                N.ptr(logits), N.ptr(baseline), N.ptr(lstm["hN"]), N.ptr(lstm["cN"]), stream),
+                "bp_atari_lstm_forward")
+        else:
+            N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), N.ptr(reward), N.ptr(last_action),
+                                             N.ptr(self.flat_params), N.ptr(logits), N.ptr(baseline),
+                                             stream), "bp_atari_forward")
         self._last_n = n
         return logits, baseline
 
-    def _backward_kernels(self, d_logits, d_baseline, reward, last_action, grads):
+    def _backward_kernels(self, d_logits, d_baseline, reward, last_action, grads, lstm: dict | None = None):
         n = d_logits.shape[0]
         b = self.buffers_for(n)
         d_logits = d_logits.contiguous().float()
         d_baseline = d_baseline.contiguous().float()
+        stream = N.stream_handle(d_logits.device)
+        if self.use_lstm:
+            N.check(N.lib().bp_atari_lstm_backward(
+                b.ref, b.lstm.ref, lstm["T1"], lstm["B"], N.ptr(d_logits), N.ptr(d_baseline),
+                N.ptr(lstm["done"]), N.ptr(self.flat_params), N.ptr(lstm["c0"]), N.ptr(grads), stream),
+                "bp_atari_lstm_backward")
+            return
         N.check(N.lib().bp_atari_backward(b.ref, n, N.ptr(d_logits), N.ptr(d_baseline), N.ptr(reward),
-                                          N.ptr(last_action), N.ptr(grads),
-                                          N.stream_handle(d_logits.device)), "bp_atari_backward")
+                                          N.ptr(last_action), N.ptr(grads), stream), "bp_atari_backward")
 
     def sample(self, logits: torch.Tensor, greedy: bool) -> torch.Tensor:
         """Gumbel-max categorical sample (training) or argmax (eval), one kernel."""
@@ -259,8 +337,15 @@ class AtariNet(nn.Module):
         return out
 
     # ------------------------------------------------------------------ upstream API
+    @property
+    def core_hidden(self) -> int:
+        return self.fc.out_features + self.num_actions + 1
+
     def initial_state(self, batch_size):
-        return tuple()
+        if not self.use_lstm:
+            return tuple()
+        dev = self.flat_params.device
+        return tuple(torch.zeros(2, batch_size, self.core_hidden, device=dev) for _ in range(2))
 
     def forward(self, inputs, core_state=()):
         x = inputs["frame"]
@@ -273,11 +358,28 @@ class AtariNet(nn.Module):
         frames = frames.contiguous()
         reward = inputs["reward"].reshape(T * B).float().contiguous()
         last_action = inputs["last_action"].reshape(T * B).to(torch.int64).contiguous()
-        if torch.is_grad_enabled():
+        state = tuple()
+        if self.use_lstm:
+            done = inputs["done"].reshape(T * B).contiguous()
+            done = done.view(torch.uint8) if done.dtype == torch.bool else (done != 0).to(torch.uint8)
+            if len(core_state) != 2:
+                raise DimensionError("LSTM core_state must be (h, c), each (2, B, hidden)")
+            h0, c0 = (s.detach().float().contiguous() for s in core_state)
+            if tuple(h0.shape) != (2, B, self.core_hidden) or tuple(c0.shape) != (2, B, self.core_hidden):
+                raise DimensionError(f"core_state shapes {tuple(h0.shape)}, expected (2, {B}, {self.core_hidden})")
+            if torch.is_grad_enabled():
+                logits, baseline, hN, cN = _AtariLstmFunction.apply(
+                    self, frames, reward, last_action, done, h0, c0, T, B, *self.parameters())
+            else:
+                lstm = dict(T1=T, B=B, done=done, h0=h0, c0=c0)
+                logits, baseline = self._forward_kernels(frames, reward, last_action, lstm=lstm)
+                hN, cN = lstm["hN"], lstm["cN"]
+            state = (hN, cN)
+        elif torch.is_grad_enabled():
             logits, baseline = _AtariFunction.apply(self, frames, reward, last_action,
                                                     *self.parameters())
         else:
             logits, baseline = self._forward_kernels(frames, reward, last_action)
         action = self.sample(logits.detach(), greedy=not self.training)
         return (dict(policy_logits=logits.view(T, B, self.num_actions), baseline=baseline.view(T, B),
-                     action=action.view(T, B)), tuple())
+                     action=action.view(T, B)), state)

@@ -1,0 +1,51 @@
+// Internal interface of the LSTM recurrent kernels (lstm.cu) used by network.cu.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bp {
+
+constexpr int kLstmU = 4;       // hidden units per CTA (4 gate rows each -> 16 W_hh rows)
+constexpr int kLstmB = 32;      // batch columns per recurrent pass (host loops over chunks)
+constexpr int kLstmKmax = 576;  // max hidden size (A <= 31 -> H = 513 + A <= 544)
+
+// Rows of every per-row tensor are t * ldb + b0 + b (time-major, full batch ldb).
+struct LstmFwdArgs {
+  int H, B, ldb, b0, T1;
+  const float* whh;           // [4H][H] f32 (torch weight_hh)
+  const float* gx;            // [rows][gx_ld] x W_ih^T + b_ih + b_hh (gate order i, f, g, o)
+  int gx_ld;
+  const uint8_t* done;        // [rows] (bool storage): state reset before step t
+  const float* h0;            // [ldb][H]
+  const float* c0;            // [ldb][H]
+  float* hx;                  // [2][H][kLstmB] exchange (per chunk)
+  float* gates;               // [rows][4H] activated i, f, g, o
+  float* cseq;                // [rows][H]
+  __nv_bfloat16* out_aug;     // [rows][aug_ld]: [h_t | 1 | 0]
+  __nv_bfloat16* hprev_aug;   // [rows][aug_ld]: [notdone_t * h_{t-1} | 1 | 0]
+  int aug_ld;
+  float* hN;                  // [ldb][H]
+  float* cN;                  // [ldb][H]
+};
+
+struct LstmBwdArgs {
+  int H, B, ldb, b0, T1;
+  const float* whh;
+  const float* gates;
+  const float* cseq;
+  const float* c0;
+  const uint8_t* done;
+  const float* dh_out;        // [rows][dh_ld] gradient w.r.t. the layer output h_t
+  int dh_ld;
+  float* part;                // [2][grid][kLstmB][Hp] recurrent partial sums
+  __nv_bfloat16* dgates;      // [rows][dg_ld] pre-activation gate gradients
+  int dg_ld;
+};
+
+int lstm_grid(int H);
+int lstm_launch_fwd(const LstmFwdArgs& a, cudaStream_t s);
+int lstm_launch_bwd(const LstmBwdArgs& a, cudaStream_t s);
+size_t lstm_part_floats(int H);
+
+}  // namespace bp

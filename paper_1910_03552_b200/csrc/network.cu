@@ -32,6 +32,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "lstm.h"
 #include "tma_host.h"
 #include "umma_gemm.cuh"
 
@@ -39,12 +40,16 @@ namespace bp {
 
 // ============================================================ param layout
 enum {
-  P_W1, P_B1, P_W2, P_B2, P_W3, P_B3, P_WFC, P_BFC, P_WP, P_BP, P_WV, P_BV, P_COUNT
+  P_W1, P_B1, P_W2, P_B2, P_W3, P_B3, P_WFC, P_BFC,
+  P_WIH0, P_WHH0, P_BIH0, P_BHH0, P_WIH1, P_WHH1, P_BIH1, P_BHH1,  // use_lstm only
+  P_WP, P_BP, P_WV, P_BV, P_COUNT
 };
 
-static void param_offsets(int A, int64_t* off) {
+static void param_offsets(int A, int lstm, int64_t* off) {
   const int64_t core = 512 + 1 + A;
+  const int64_t g = lstm ? 4 * core * core : 0, b = lstm ? 4 * core : 0;
   const int64_t sizes[P_COUNT] = {256 * 32, 32, 512 * 64, 64, 576 * 64, 64, 3136 * 512, 512,
+                                  g, g, b, b, g, g, b, b,
                                   A * core, A, core, 1};
   int64_t o = 0;
   for (int i = 0; i < P_COUNT; ++i) {
@@ -468,18 +473,18 @@ extern "C" int bp_gemm_shift_test(const void* A, const void* B, float* Cout, int
 }
 
 extern "C" int64_t bp_atari_param_count(int num_actions, int use_lstm) {
-  if (num_actions < 1 || num_actions > 31 || use_lstm) return -1;
+  if (num_actions < 1 || num_actions > 31) return -1;
   int64_t off[P_COUNT + 1];
-  param_offsets(num_actions, off);
+  param_offsets(num_actions, use_lstm, off);
   return off[P_COUNT];
 }
 
 extern "C" int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* offsets) {
-  if (num_actions < 1 || num_actions > 31 || use_lstm || !offsets) {
-    set_error("atari: num_actions must be in [1, 31] (LSTM core: separate entry points)");
+  if (num_actions < 1 || num_actions > 31 || !offsets) {
+    set_error("atari: num_actions must be in [1, 31]");
     return BP_ERR_ARG;
   }
-  param_offsets(num_actions, offsets);
+  param_offsets(num_actions, use_lstm, offsets);
   return BP_OK;
 }
 
@@ -502,20 +507,17 @@ static int check_net(const BpAtariNet* net, int n) {
 extern "C" int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stream) {
   if (int e = check_net(net, 1)) return e;
   int64_t off[P_COUNT + 1];
-  param_offsets(net->num_actions, off);
+  param_offsets(net->num_actions, net->use_lstm, off);
   cast_bf16_kernel<<<296, 256, 0, (cudaStream_t)stream>>>(
       params, reinterpret_cast<__nv_bfloat16*>(net->wbf), off[P_COUNT]);
   return check_launch("cast_bf16_kernel");
 }
 
-extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
-                                const float* reward, const int64_t* last_action, const float* params,
-                                float* logits, float* baseline, void* stream) {
-  if (int e = check_net(net, n)) return e;
-  cudaStream_t s = (cudaStream_t)stream;
+// frames -> conv torso -> fc -> augmented core [n][576] (net->core)
+static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
+                         const int64_t* last_action, const float* params, const int64_t* off,
+                         cudaStream_t s) {
   const int A = net->num_actions;
-  int64_t off[P_COUNT + 1];
-  param_offsets(A, off);
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
@@ -612,68 +614,89 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
     g.r_img = kCoreW;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 6. heads: core [n, 576] x Whf [32, 576] -> logits [n, A], baseline [n]
-  {
-    if ((rc = make_tmap(&ta, net->core, n, kCoreW, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 32, 128))) return rc;
-    GemmArgs g = base_args();
-    g.m_tiles = (n + 127) / 128;
-    g.n_tiles = 1;
-    g.num_kb = g.kb_per_split = kCoreW / 64;
-    g.a_cb = kCoreW / 64;
-    g.N = 32;
-    g.M = n;
-    g.heads = 1;
-    g.A = A;
-    g.logits = logits;
-    g.baseline = baseline;
-    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s))) return rc;
-  }
   return BP_OK;
 }
 
-extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits,
-                                 const float* d_baseline, const float* reward,
-                                 const int64_t* last_action, float* grads, void* stream) {
-  (void)reward;
-  (void)last_action;  // (their contribution to the heads gradient comes from the augmented core)
+// heads: head_in [n, 576] ([core | 1 | 0]) x Whf [32, 576] -> logits [n, A], baseline [n]
+static int heads_forward(const BpAtariNet* net, int n, const void* head_in, float* logits, float* baseline,
+                         cudaStream_t s) {
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_tmap(&ta, head_in, n, kCoreW, 64, 128, 128))) return rc;
+  if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 32, 128))) return rc;
+  GemmArgs g = base_args();
+  g.m_tiles = (n + 127) / 128;
+  g.n_tiles = 1;
+  g.num_kb = g.kb_per_split = kCoreW / 64;
+  g.a_cb = kCoreW / 64;
+  g.N = 32;
+  g.M = n;
+  g.heads = 1;
+  g.A = net->num_actions;
+  g.logits = logits;
+  g.baseline = baseline;
+  return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s);
+}
+
+extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
+                                const float* reward, const int64_t* last_action, const float* params,
+                                float* logits, float* baseline, void* stream) {
   if (int e = check_net(net, n)) return e;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int A = net->num_actions;
-  int64_t off[P_COUNT + 1];
-  param_offsets(A, off);
-  NetPlan P;
-  make_plan(n, g_num_sms, &P);
-  if (P.total_floats * sizeof(float) > net->ws_bytes) {
-    set_error("atari backward: workspace %zu < %zu bytes", net->ws_bytes, P.total_floats * sizeof(float));
+  if (net->use_lstm) {
+    set_error("atari: LSTM net -> bp_atari_lstm_forward");
     return BP_ERR_ARG;
   }
-  float* ws = reinterpret_cast<float*>(net->ws);
-  const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t off[P_COUNT + 1];
+  param_offsets(net->num_actions, 0, off);
+  int rc;
+  if ((rc = torso_forward(net, n, frames, reward, last_action, params, off, s))) return rc;
+  return heads_forward(net, n, net->core, logits, baseline, s);
+}
+
+// G = [d_logits | d_baseline | 0] bf16, then the heads data-gradient:
+//   dh_f32 == nullptr: d_fc = (G x Whf[:, :512]) * relu mask, colsum -> d bfc partials
+//   dh_f32 != nullptr: dh_f32 [n][576] = G x Whf (unmasked, f32: the LSTM output gradient)
+static int heads_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
+                          const NetPlan& P, float* ws, float* dh_f32, cudaStream_t s) {
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
-  CUtensorMap ta, tb;
-  // 1. G = [d_logits | d_baseline | 0] bf16
-  pack_g_kernel<<<(n * 8 + 255) / 256, 256, 0, s>>>(d_logits, d_baseline, bf(net->g), n, A);
+  pack_g_kernel<<<(n * 8 + 255) / 256, 256, 0, s>>>(d_logits, d_baseline, bf(net->g), n, net->num_actions);
   if ((rc = check_launch("pack_g_kernel"))) return rc;
-  // 2. heads dgrad: d_fc = (G [n,64] x Whf[:, :512]) * (h > 0); colsum -> d bfc
-  {
-    if ((rc = make_tmap(&ta, net->g, n, 64, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 64, 128))) return rc;  // MN-major, rows >= 32 OOB = 0
-    GemmArgs g = base_args();
-    g.m_tiles = (n + 127) / 128;
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap(&ta, net->g, n, 64, 64, 128, 128))) return rc;
+  if ((rc = make_tmap(&tb, net->whf, 32, kCoreW, 64, 64, 128))) return rc;  // MN-major, rows >= 32 OOB = 0
+  GemmArgs g = base_args();
+  g.m_tiles = (n + 127) / 128;
+  g.num_kb = g.kb_per_split = 1;
+  g.M = n;
+  if (dh_f32) {
+    g.n_tiles = kCoreW / 64;
+    g.N = kCoreW;
+    g.out_f32 = 1;
+    g.out = dh_f32;
+    g.r_img = kCoreW;
+  } else {
     g.n_tiles = 8;
-    g.num_kb = g.kb_per_split = 1;
     g.N = 512;
-    g.M = n;
     g.mask_bits = reinterpret_cast<const uint32_t*>(net->mc);
     g.mask_ld = kCoreW;
     g.out = net->d_fc;
     g.r_img = 512;
     g.colsum = ws + P.cs_off[3];
-    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 3. fc dgrad: d_pre3 (conv3 9x9 grid) = (d_fc [n,512] x Wfc [512,3136]) * (X3 > 0); colsum -> d b3
+  return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
+}
+
+// d_fc -> conv torso data / weight gradients, heads weight gradient (A operand head_in),
+// deterministic finalize of every partial into grads
+static int torso_backward(const BpAtariNet* net, int n, const void* head_in, float* grads, const int64_t* off,
+                          const NetPlan& P, float* ws, cudaStream_t s) {
+  const int A = net->num_actions;
+  const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
+  int rc;
+  CUtensorMap ta, tb;
+  // fc dgrad: d_pre3 (conv3 9x9 grid) = (d_fc [n,512] x Wfc [512,3136]) * (X3 > 0); colsum -> d b3
   {
     if ((rc = make_tmap(&ta, net->d_fc, n, 512, 64, 128, 128))) return rc;
     if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, 64, 128))) return rc;
@@ -691,7 +714,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.colsum = ws + P.cs_off[2];
     if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 4. conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
+  // conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
   {
     const long long R = (long long)n * 81;
     GemmArgs g = base_args();
@@ -714,7 +737,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.colsum = ws + P.cs_off[1];
     if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
-  // 5. conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
+  // conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
   {
     const long long R = (long long)n * 100;
     GemmArgs g = base_args();
@@ -738,7 +761,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.colsum = ws + P.cs_off[0];
     if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
-  // 6. weight gradients
+  // weight gradients
   auto wgrad = [&](int i, const void* X, long long xrows, int xcols, int atoms_per_shift, int nshifts,
                    const int* offs, const void* dY, int ncols) -> int {
     const WgPlan& w = P.wg[i];
@@ -776,7 +799,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
       for (int dx = 0; dx < 3; ++dx) o3[dy * 3 + dx] = dy * 9 + dx;
     if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
     const int o0[1] = {0};
-    if ((rc = wgrad(3, net->core, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
+    if ((rc = wgrad(3, head_in, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
   }
   // fc weight gradient with swapped roles: D[o][k] = sum_n d_fc[n][o] X3[n][k] -> grads, no split
   {
@@ -795,7 +818,7 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     g.r_img = 3136;
     if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
-  // 7. deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
+  // deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
   {
     FinArgs f;
     memset(&f, 0, sizeof(f));
@@ -828,6 +851,259 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
     if ((rc = check_launch("finalize_kernel"))) return rc;
   }
   return BP_OK;
+}
+
+static int plan_for(const BpAtariNet* net, int n, NetPlan* P) {
+  make_plan(n, g_num_sms, P);
+  if (P->total_floats * sizeof(float) > net->ws_bytes) {
+    set_error("atari backward: workspace %zu < %zu bytes", net->ws_bytes, P->total_floats * sizeof(float));
+    return BP_ERR_ARG;
+  }
+  return BP_OK;
+}
+
+extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits,
+                                 const float* d_baseline, const float* reward,
+                                 const int64_t* last_action, float* grads, void* stream) {
+  (void)reward;
+  (void)last_action;  // (their contribution to the heads gradient comes from the augmented core)
+  if (int e = check_net(net, n)) return e;
+  if (net->use_lstm) {
+    set_error("atari: LSTM net -> bp_atari_lstm_backward");
+    return BP_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t off[P_COUNT + 1];
+  param_offsets(net->num_actions, 0, off);
+  NetPlan P;
+  int rc;
+  if ((rc = plan_for(net, n, &P))) return rc;
+  float* ws = reinterpret_cast<float*>(net->ws);
+  if ((rc = heads_backward(net, n, d_logits, d_baseline, P, ws, nullptr, s))) return rc;
+  return torso_backward(net, n, net->core, grads, off, P, ws, s);
+}
+
+// ============================================================ LSTM core
+// input projection / weight-gradient operand: wih [G4][576] = [W_ih | b_ih + b_hh | 0], rows >= 4H zero
+__global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float* __restrict__ bih,
+                                     const float* __restrict__ bhh, __nv_bfloat16* __restrict__ dst, int H,
+                                     int G4) {
+  const int H4 = 4 * H;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)G4 * kCoreW;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / kCoreW), k = (int)(i % kCoreW);
+    float v = 0.f;
+    if (r < H4) v = k < H ? wih[(size_t)r * H + k] : (k == H ? bih[r] + bhh[r] : 0.f);
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// weight-gradient GEMM outputs [G4][576] -> torch-layout grads of one layer
+__global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* __restrict__ phh,
+                                    float* __restrict__ gwih, float* __restrict__ gwhh,
+                                    float* __restrict__ gbih, float* __restrict__ gbhh, int H) {
+  const long long n = 4LL * H * H;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / H, k = i % H;
+    gwih[i] = pih[r * kCoreW + k];
+    gwhh[i] = phh[r * kCoreW + k];
+    if (k == 0) {
+      const float b = pih[r * kCoreW + H];
+      gbih[r] = b;
+      gbhh[r] = b;
+    }
+  }
+}
+
+// d_fc [n][512] bf16 = dcore[:, :512] * relu mask; bias-gradient partials per 32-row group
+__global__ void __launch_bounds__(256) lstm_dfc_kernel(const float* __restrict__ dcore,
+                                                       const uint32_t* __restrict__ mc,
+                                                       __nv_bfloat16* __restrict__ d_fc,
+                                                       float* __restrict__ colsum, int n) {
+  const int grp = blockIdx.x;  // rows [32*grp, 32*grp + 32)
+  for (int c = threadIdx.x; c < 512; c += 256) {
+    float s = 0.f;
+    for (int i = 0; i < 32; ++i) {
+      const int m = grp * 32 + i;
+      if (m >= n) break;
+      const size_t bit = (size_t)m * kCoreW + c;
+      const float v = ((mc[bit >> 5] >> (bit & 31)) & 1u) ? dcore[(size_t)m * kCoreW + c] : 0.f;
+      const __nv_bfloat16 vb = __float2bfloat16_rn(v);
+      d_fc[(size_t)m * 512 + c] = vb;
+      s += v;
+    }
+    colsum[(size_t)grp * 512 + c] = s;
+  }
+}
+
+extern "C" size_t bp_lstm_partial_floats(int hidden) { return lstm_part_floats(hidden); }
+
+static int lstm_g4(int H) { return (4 * H + 127) & ~127; }
+
+static int check_lstm(const BpAtariNet* net, const BpLstmCore* core, int T1, int B) {
+  if (int e = check_net(net, T1 * B)) return e;
+  if (!net->use_lstm || !core || core->hidden != 513 + net->num_actions || T1 * B > core->max_rows) {
+    set_error("lstm: net / core mismatch (use_lstm %d, hidden %d, rows %d of %d)", net->use_lstm,
+              core ? core->hidden : -1, T1 * B, core ? core->max_rows : -1);
+    return BP_ERR_ARG;
+  }
+  return BP_OK;
+}
+
+extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                     const uint8_t* frames, const float* reward, const int64_t* last_action,
+                                     const uint8_t* done, const float* params, const float* h0,
+                                     const float* c0, float* logits, float* baseline, float* hN, float* cN,
+                                     void* stream) {
+  if (int e = check_lstm(net, core, T1, B)) return e;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = T1 * B, H = core->hidden, G4 = lstm_g4(H);
+  int64_t off[P_COUNT + 1];
+  param_offsets(net->num_actions, 1, off);
+  int rc;
+  if ((rc = torso_forward(net, n, frames, reward, last_action, params, off, s))) return rc;
+  __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(core->wih);
+  const size_t wsz = (size_t)G4 * kCoreW;
+  for (int l = 0; l < 2; ++l) {
+    const int pw = l ? P_WIH1 : P_WIH0, pb = l ? P_BIH1 : P_BIH0, pc = l ? P_BHH1 : P_BHH0;
+    pack_lstm_wih_kernel<<<148, 512, 0, s>>>(params + off[pw], params + off[pb], params + off[pc], wih + l * wsz,
+                                             H, G4);
+    if ((rc = check_launch("pack_lstm_wih_kernel"))) return rc;
+  }
+  auto bfp = [&](void* base, int l) {
+    return reinterpret_cast<__nv_bfloat16*>(base) + (size_t)l * core->max_rows * kCoreW;
+  };
+  for (int l = 0; l < 2; ++l) {
+    // gx [n][G4] = x_aug [n][576] . wih^T (biases through the ones column)
+    CUtensorMap ta, tb;
+    const void* x = l ? (const void*)bfp(core->out, 0) : net->core;
+    if ((rc = make_tmap(&ta, x, n, kCoreW, 64, 128, 128))) return rc;
+    if ((rc = make_tmap(&tb, wih + l * wsz, G4, kCoreW, 64, 64, 128))) return rc;
+    GemmArgs g = base_args();
+    g.m_tiles = (n + 127) / 128;
+    g.n_tiles = G4 / 64;
+    g.num_kb = g.kb_per_split = kCoreW / 64;
+    g.a_cb = kCoreW / 64;
+    g.N = G4;
+    g.M = n;
+    g.out_f32 = 1;
+    g.out = core->gx;
+    g.r_img = G4;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    for (int b0 = 0; b0 < B; b0 += kLstmB) {
+      LstmFwdArgs a;
+      a.H = H;
+      a.B = B - b0 < kLstmB ? B - b0 : kLstmB;
+      a.ldb = B;
+      a.b0 = b0;
+      a.T1 = T1;
+      a.whh = params + off[l ? P_WHH1 : P_WHH0];
+      a.gx = core->gx;
+      a.gx_ld = G4;
+      a.done = done;
+      a.h0 = h0 + (size_t)l * B * H;
+      a.c0 = c0 + (size_t)l * B * H;
+      a.hx = core->hx;
+      a.gates = core->gates + (size_t)l * core->max_rows * 4 * H;
+      a.cseq = core->cseq + (size_t)l * core->max_rows * H;
+      a.out_aug = bfp(core->out, l);
+      a.hprev_aug = bfp(core->hprev, l);
+      a.aug_ld = kCoreW;
+      a.hN = hN + (size_t)l * B * H;
+      a.cN = cN + (size_t)l * B * H;
+      if ((rc = lstm_launch_fwd(a, s))) return rc;
+    }
+  }
+  return heads_forward(net, n, bfp(core->out, 1), logits, baseline, s);
+}
+
+extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                      const float* d_logits, const float* d_baseline, const uint8_t* done,
+                                      const float* params, const float* c0, float* grads, void* stream) {
+  if (int e = check_lstm(net, core, T1, B)) return e;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = T1 * B, H = core->hidden, G4 = lstm_g4(H);
+  int64_t off[P_COUNT + 1];
+  param_offsets(net->num_actions, 1, off);
+  NetPlan P;
+  int rc;
+  if ((rc = plan_for(net, n, &P))) return rc;
+  float* ws = reinterpret_cast<float*>(net->ws);
+  auto bfp = [&](void* base, int l) {
+    return reinterpret_cast<__nv_bfloat16*>(base) + (size_t)l * core->max_rows * kCoreW;
+  };
+  const __nv_bfloat16* wih = reinterpret_cast<const __nv_bfloat16*>(core->wih);
+  const size_t wsz = (size_t)G4 * kCoreW;
+  // d(out[1]) [n][576] f32 from the heads
+  if ((rc = heads_backward(net, n, d_logits, d_baseline, P, ws, core->dh, s))) return rc;
+  for (int l = 1; l >= 0; --l) {
+    float* dh_in = l == 1 ? core->dh : core->dx;   // gradient w.r.t. this layer's output
+    float* dx_out = l == 1 ? core->dx : core->dh;  // gradient w.r.t. this layer's input
+    for (int b0 = 0; b0 < B; b0 += kLstmB) {
+      LstmBwdArgs a;
+      a.H = H;
+      a.B = B - b0 < kLstmB ? B - b0 : kLstmB;
+      a.ldb = B;
+      a.b0 = b0;
+      a.T1 = T1;
+      a.whh = params + off[l ? P_WHH1 : P_WHH0];
+      a.gates = core->gates + (size_t)l * core->max_rows * 4 * H;
+      a.cseq = core->cseq + (size_t)l * core->max_rows * H;
+      a.c0 = c0 + (size_t)l * B * H;
+      a.done = done;
+      a.dh_out = dh_in;
+      a.dh_ld = kCoreW;
+      a.part = core->part;
+      a.dgates = reinterpret_cast<__nv_bfloat16*>(core->dgates);
+      a.dg_ld = G4;
+      if ((rc = lstm_launch_bwd(a, s))) return rc;
+    }
+    CUtensorMap ta, tb;
+    // weight gradients: D[r][k] = sum_rows dgates[row][r] * X[row][k], X = layer input / previous state
+    for (int w = 0; w < 2; ++w) {
+      const void* X = w == 0 ? (l ? (const void*)bfp(core->out, 0) : net->core) : (const void*)bfp(core->hprev, l);
+      if ((rc = make_tmap(&ta, core->dgates, n, G4, 64, 64, 128))) return rc;
+      if ((rc = make_tmap(&tb, X, n, kCoreW, 64, 64, 128))) return rc;
+      GemmArgs g = base_args();
+      g.m_tiles = G4 / 128;
+      g.n_tiles = kCoreW / 64;
+      g.num_kb = g.kb_per_split = (n + 63) / 64;
+      g.a_atoms_per_shift = G4 / 64;
+      g.a_nshifts = 1;
+      g.N = kCoreW;
+      g.M = G4;
+      g.out_f32 = 1;
+      g.out = core->wpart + (size_t)w * G4 * kCoreW;
+      g.r_img = kCoreW;
+      if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    }
+    // input gradient: dx [n][576] = dgates [n][G4] . wih [G4][576]
+    {
+      if ((rc = make_tmap(&ta, core->dgates, n, G4, 64, 128, 128))) return rc;
+      if ((rc = make_tmap(&tb, wih + l * wsz, G4, kCoreW, 64, 64, 128))) return rc;
+      GemmArgs g = base_args();
+      g.m_tiles = (n + 127) / 128;
+      g.n_tiles = kCoreW / 64;
+      g.num_kb = g.kb_per_split = G4 / 64;
+      g.a_cb = G4 / 64;
+      g.N = kCoreW;
+      g.M = n;
+      g.out_f32 = 1;
+      g.out = dx_out;
+      g.r_img = kCoreW;
+      if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    }
+    lstm_scatter_kernel<<<296, 256, 0, s>>>(core->wpart, core->wpart + (size_t)G4 * kCoreW,
+                                            grads + off[l ? P_WIH1 : P_WIH0], grads + off[l ? P_WHH1 : P_WHH0],
+                                            grads + off[l ? P_BIH1 : P_BIH0], grads + off[l ? P_BHH1 : P_BHH0], H);
+    if ((rc = check_launch("lstm_scatter_kernel"))) return rc;
+  }
+  // layer-0 input gradient (core->dh) -> d_fc (relu mask) + bias partials for dbfc
+  lstm_dfc_kernel<<<P.cs_rows[3], 256, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
+                                               reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);
+  if ((rc = check_launch("lstm_dfc_kernel"))) return rc;
+  return torso_backward(net, n, bfp(core->out, 1), grads, off, P, ws, s);
 }
 
 // ============================================================ action sampling

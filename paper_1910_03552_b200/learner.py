@@ -7,6 +7,7 @@ optimizer, scheduler, lock)` [upstream, not vendored] with the same signature.
 
 One step = (all on the current CUDA stream, no host sync until stats are read)
   1. AtariNet forward on (T+1)*B frames          bp_atari_forward   (tcgen05)
+     (LSTM core: bp_atari_lstm_forward -- persistent recurrent kernels)
   2. fused V-trace + 3 losses + d_logits/d_base  bp_learner_loss_f32
   3. AtariNet backward -> flat f32 gradients     bp_atari_backward  (tcgen05)
   4. [DP] NCCL all-reduce(SUM) of the flat gradient buffer (torch.distributed)
@@ -58,6 +59,13 @@ class FusedLearner:
         self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
         self.pg = process_group
         model.buffers_for(self.n)
+        # LSTM core: the initial agent state is staged into fixed buffers (graph inputs)
+        self.lstm = None
+        if getattr(model, "use_lstm", False):
+            shape = (2, batch_size, model.core_hidden)
+            self.lstm = dict(T1=unroll_length + 1, B=batch_size,
+                             h0=torch.zeros(shape, device=dev), c0=torch.zeros(shape, device=dev),
+                             hN=torch.empty(shape, device=dev), cN=torch.empty(shape, device=dev))
         # CUDA graphs: one captured step per (batch buffer set, optimizer); see step()
         self.use_graphs = True
         self.kernels_per_step = 0
@@ -73,7 +81,7 @@ class FusedLearner:
         keys = ("frame", "reward", "done", "policy_logits", "action", "last_action")
         return tuple(batch[k].data_ptr() for k in keys) + (id(optimizer),)
 
-    def step(self, batch, optimizer=None, scheduler=None):
+    def step(self, batch, optimizer=None, scheduler=None, initial_agent_state=()):
         """Enqueue one learner step on the current stream; returns the device loss vector.
 
         With `use_graphs` (default) the whole step -- forward, fused loss,
@@ -81,7 +89,15 @@ class FusedLearner:
         set of batch buffers (e.g. the two DeviceInfeed slots) as a CUDA graph and
         replayed, so host launch overhead leaves the critical path.  The first
         call per buffer set runs eagerly (warm-up), the second captures.
+        LSTM nets copy `initial_agent_state` (h, c) into the staged state buffers first.
         """
+        if self.lstm is not None:
+            if len(initial_agent_state) == 2:
+                self.lstm["h0"].copy_(initial_agent_state[0])
+                self.lstm["c0"].copy_(initial_agent_state[1])
+            else:
+                self.lstm["h0"].zero_()
+                self.lstm["c0"].zero_()
         graphable = (self.use_graphs and (self.pg is None or self._pg_is_nccl()) and
                      (optimizer is None or (isinstance(optimizer, RMSprop) and
                                             optimizer.flat_params.data_ptr() ==
@@ -125,10 +141,15 @@ class FusedLearner:
         A = m.num_actions
         reward = batch["reward"]
         last_action = batch["last_action"]
+        lstm = None
+        if self.lstm is not None:
+            done = batch["done"].reshape(n)
+            lstm = dict(self.lstm, done=done.view(torch.uint8) if done.dtype == torch.bool else done)
         # 1. forward (the bf16 operand mirror is refreshed by the fused optimiser below)
         m._forward_kernels(frames.reshape(n, *m.observation_shape), reward.reshape(n),
                            last_action.reshape(n), logits=self.logits, baseline=self.baseline,
-                           repack=None)  # packs only if stale (first step, load_state_dict, ...)
+                           repack=None,  # packs only if stale (first step, load_state_dict, ...)
+                           lstm=lstm)
         # 2. fused V-trace + losses + gradients w.r.t. logits / baseline
         self.loss(self.logits[:T * B].view(T, B, A), self.baseline.view(T + 1, B),
                   batch["policy_logits"][1:], batch["action"][1:], reward[1:], batch["done"][1:],
@@ -136,7 +157,7 @@ class FusedLearner:
                   d_baseline=self.d_baseline.view(T + 1, B), losses=self.losses)
         # 3. backward into the flat gradient buffer
         m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
-                            m.flat_grads)
+                            m.flat_grads, lstm=lstm)
         # 4. data-parallel over B: the losses are sums over (T, B) (vtrace.py:194-196), so
         #    the full-batch gradient is the SUM of the shard gradients (one all-reduce of the
         #    flat f32 buffer); the loss scalars are summed too, for the stats
@@ -190,7 +211,7 @@ def learn(flags, actor_model, model, batch, initial_agent_state, optimizer, sche
         L = fl.get(key)
         if L is None:
             L = fl[key] = FusedLearner(model, flags, T1 - 1, B, process_group)
-        L.step(batch, optimizer, scheduler)
+        L.step(batch, optimizer, scheduler, initial_agent_state)
         stats = L.stats(batch)
         if actor_model is not None and actor_model is not model:
             actor_model.load_state_dict(model.state_dict())
