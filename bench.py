@@ -191,6 +191,56 @@ def kernel_breakdown(L, batch, opt, iters=10):
     return out
 
 
+def bench_lstm(dev, steps, warmup, flush, timer):
+    """configs[2]: AtariNet with the LSTM core, learner step T=80 B=32 A=18 + RMSprop
+    (graph-replayed, L2 flushed before every timed step) and its phase split."""
+    from paper_1910_03552_b200 import learner, optim
+    from paper_1910_03552_b200.atari_net import AtariNet
+
+    T, B, A = 80, 32, 18
+    torch.manual_seed(4321)
+    model = AtariNet(num_actions=A, use_lstm=True, device=dev)
+    opt = optim.RMSprop(model.parameters(), lr=FLAGS["learning_rate"], alpha=FLAGS["alpha"],
+                        eps=FLAGS["epsilon"])
+    batch = make_batch(T, B, A, dev, seed=77)
+    state = model.initial_state(B)
+    L = learner.FusedLearner(model, FLAGS, T, B)
+    for _ in range(max(3, warmup)):
+        L.step(batch, opt, None, state)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    times = []
+    for _ in range(steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        L.step(batch, opt, None, state)
+        e1.record(s)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    step_s = statistics.mean(times)
+    n = (T + 1) * B
+    lstm = dict(L.lstm, done=batch["done"].reshape(n).view(torch.uint8))
+    frames = batch["frame"].reshape(n, 4, 84, 84)
+
+    def fwd():
+        model._forward_kernels(frames, batch["reward"].reshape(n), batch["last_action"].reshape(n),
+                               logits=L.logits, baseline=L.baseline, repack=False, lstm=lstm)
+
+    def bwd():
+        model._backward_kernels(L.d_logits, L.d_baseline, batch["reward"].reshape(n),
+                                batch["last_action"].reshape(n), model.flat_grads, lstm=lstm)
+
+    phases = {k: timer.time(f, iters=10, warmup=2, flush=True, graph=True)["median_s"]
+              for k, f in (("forward", fwd), ("backward", bwd))}
+    return {"workload": "configs[2]: AtariNet + 2-layer LSTM core learner step + RMSprop",
+            "T": T, "B": B, "num_actions": A, "value": T * B / step_s, "unit": "env-frames/s",
+            "ms_per_step": step_s * 1e3, "phase_seconds": phases,
+            "recurrence": "persistent cooperative kernels, one grid barrier per step "
+                          "(2 layers x 81 steps forward, 2 x 81 backward)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -367,6 +417,10 @@ def main():
                "ms": ri["median_s"] * 1e3, "obs_per_s": 1024 / ri["median_s"],
                "tflops": inf_flops / ri["median_s"] / 1e12}
 
+    lstm_line = None
+    if rank == 0:
+        lstm_line = bench_lstm(dev, 10, 3, flush, timer)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(T, B, A, steps=3, warmup=1, budget_s=30.0)
@@ -385,7 +439,7 @@ def main():
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
             "roofline": roofline, "vtrace_roofline": vt_roof,
             "learner_loss_kernel_s": ll["median_s"], "vtrace_sweep": vt_sweep,
-            "inference": inf,
+            "inference": inf, "lstm": lstm_line,
             "cpu_baseline": cpu, "clocks": clk.summary(),
             "stats_last": {k: stats[k] for k in ("total_loss", "pg_loss", "baseline_loss",
                                                  "entropy_loss")},

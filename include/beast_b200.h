@@ -226,6 +226,9 @@ typedef struct BpLstmCore {
   float* wpart;   /* [2][G4][576] f32 weight-gradient GEMM outputs           */
 } BpLstmCore;
 size_t bp_lstm_partial_floats(int hidden);
+/* Diagnostics: per-step %globaltimer trace of CTA 0 of the recurrent kernels into
+ * buf (device u64 [2][T1][4]: forward phases, then backward phases); NULL disables. */
+int bp_lstm_trace(void* buf);
 /* Forward of T1*B frames through torso + LSTM core + heads.  done [T1*B] u8;
  * h0, c0 [2][B][H] f32 initial state (layer-major, torch (num_layers, B, H));
  * hN, cN [2][B][H] receive the final state.  B is split into recurrent passes of <= 32. */

@@ -37,60 +37,76 @@ int lstm_grid(int H) { return (H + kLstmU - 1) / kLstmU; }
 size_t lstm_part_floats(int H) { return (size_t)2 * lstm_grid(H) * kLstmB * lstm_hp(H); }
 
 // --------------------------------------------------------------------------- forward
+// optional per-step %globaltimer trace of CTA 0 (diagnostics: bp_lstm_trace)
+__device__ unsigned long long* g_lstm_trace = nullptr;
+
+BP_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwdArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ float4 sm4[];
   float* sm = reinterpret_cast<float*>(sm4);
+  __shared__ uint64_t hbar;
   const int H = a.H, B = a.B, H4 = 4 * H;
   const int KP = lstm_kp(H), KS = KP / 8;
   const int u0 = blockIdx.x * kLstmU;
   const int nu = min(kLstmU, H - u0);
   float* wt = sm;                      // [KP][16]  W_hh rows (gate*4 + u), k-major
-  float* ht = wt + KP * kRows;         // [KP][32]  h'_{t-1}, k-major
+  float* ht = wt + KP * kRows;         // [KP][32]  h_{t-1} (reset applied to the sums), k-major
   float* red = ht + KP * kLstmB;       // [8][16][32] per-warp partial pre-gates
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_lstm_trace : nullptr;
+  if (tid == 0) {
+    mbar_init(&hbar, 1);
+    fence_mbar_init();
+  }
   for (int i = tid; i < KP * kRows; i += kLstmThreads) {
     const int k = i / kRows, r = i % kRows;
     const int gate = r / kLstmU, u = r % kLstmU;
     wt[i] = (u < nu && k < H) ? a.whh[(size_t)(gate * H + u0 + u) * H + k] : 0.f;
   }
   for (int i = H * kLstmB + tid; i < KP * kLstmB; i += kLstmThreads) ht[i] = 0.f;
+  // h0 (transposed to [k][b]; batch columns >= B zero)
+  for (int i = tid; i < H * kLstmB; i += kLstmThreads) {
+    const int k = i / kLstmB, b = i % kLstmB;
+    ht[i] = b < B ? a.h0[(size_t)(a.b0 + b) * H + k] : 0.f;
+  }
   const int ou = tid / kLstmB, ob = tid % kLstmB;
   const bool owner = tid < kLstmU * kLstmB && ou < nu && ob < B;
   const int j = u0 + ou;
   float c = 0.f, hown = 0.f;
+  // the owner's per-step inputs are loaded one step ahead (off the critical path)
+  float gxn[4] = {0.f, 0.f, 0.f, 0.f};
+  bool donen = false;
   if (owner) {
     c = a.c0[(size_t)(a.b0 + ob) * H + j];
     hown = a.h0[(size_t)(a.b0 + ob) * H + j];
+    const size_t row = (size_t)a.b0 + ob;
+#pragma unroll
+    for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[row * a.gx_ld + gate * H + j];
+    donen = a.done[row];
   }
-  // the copy thread handles batch columns b4..b4+3 for every k it touches
-  const int b4 = (tid & 7) * 4;
   const int rg = lane >> 3, bg = lane & 7;
+  uint32_t hphase = 0;
+  __syncthreads();
   for (int t = 0; t < a.T1; ++t) {
     const size_t trow = (size_t)t * a.ldb + a.b0;
-    float nd4[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) nd4[q] = (b4 + q < B && !a.done[trow + b4 + q]) ? 1.f : 0.f;
-    if (t == 0) {
-      for (int i4 = tid; i4 < H * 8; i4 += kLstmThreads) {
-        const int k = i4 >> 3;
-        float v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = nd4[q] != 0.f ? a.h0[(size_t)(a.b0 + b4 + q) * H + k] : 0.f;
-        reinterpret_cast<float4*>(ht)[i4] = make_float4(v[0], v[1], v[2], v[3]);
+    if (trace) trace[t * 4 + 0] = gtimer();
+    if (t > 0) {  // h_{t-1} of every unit: one bulk copy of the exchange buffer
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        fence_proxy_async_smem();
+        mbar_expect_tx(&hbar, (uint32_t)(H * kLstmB * sizeof(float)));
+        bulk_g2s(ht, a.hx + (size_t)((t - 1) & 1) * H * kLstmB, (uint32_t)(H * kLstmB * sizeof(float)), &hbar);
       }
-    } else {
-      const float4* src = reinterpret_cast<const float4*>(a.hx + (size_t)((t - 1) & 1) * H * kLstmB);
-      for (int i4 = tid; i4 < H * 8; i4 += kLstmThreads) {
-        float4 v = __ldcg(src + i4);
-        v.x *= nd4[0];
-        v.y *= nd4[1];
-        v.z *= nd4[2];
-        v.w *= nd4[3];
-        reinterpret_cast<float4*>(ht)[i4] = v;
-      }
+      mbar_wait_parity(&hbar, hphase);
+      hphase ^= 1;
     }
-    __syncthreads();
+    if (trace) trace[t * 4 + 1] = gtimer();
     {
       float acc[4][4];
 #pragma unroll
@@ -116,18 +132,25 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwd
             make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
     }
     __syncthreads();
+    if (trace) trace[t * 4 + 2] = gtimer();
     if (owner) {
       const size_t row = trow + ob;
-      const float* gx = a.gx + row * a.gx_ld;
+      // reset: W_hh (notdone_t * h_{t-1}) = notdone_t * (W_hh h_{t-1})
+      const float nd = donen ? 0.f : 1.f;
       float z[4];
 #pragma unroll
       for (int gate = 0; gate < 4; ++gate) {
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += red[((size_t)w * kRows + gate * kLstmU + ou) * kLstmB + ob];
-        z[gate] = s + gx[gate * H + j];
+        z[gate] = nd * s + gxn[gate];
       }
-      const float nd = a.done[row] ? 0.f : 1.f;
+      if (t + 1 < a.T1) {  // next step's inputs
+        const size_t nrow = row + a.ldb;
+#pragma unroll
+        for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[nrow * a.gx_ld + gate * H + j];
+        donen = a.done[nrow];
+      }
       a.hprev_aug[row * a.aug_ld + j] = __float2bfloat16_rn(nd * hown);
       const float ig = sigm(z[0]), fg = sigm(z[1]), gg = tanhf(z[2]), og = sigm(z[3]);
       c = fg * (nd * c) + ig * gg;
@@ -138,7 +161,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwd
       act[2 * H + j] = gg;
       act[3 * H + j] = og;
       a.cseq[row * H + j] = c;
-      a.hx[(size_t)(t & 1) * H * kLstmB + (size_t)j * kLstmB + ob] = h;
+      __stcg(a.hx + (size_t)(t & 1) * H * kLstmB + (size_t)j * kLstmB + ob, h);
       a.out_aug[row * a.aug_ld + j] = __float2bfloat16_rn(h);
       hown = h;
       if (t == a.T1 - 1) {
@@ -151,6 +174,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwd
       a.out_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
       a.hprev_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
     }
+    if (trace) trace[t * 4 + 3] = gtimer();
     grid.sync();
   }
 }
@@ -167,6 +191,8 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(const LstmBwd
   float* zs = w + kRows * HP;        // [16][32]  own dz_{t+1}
   float4* red = reinterpret_cast<float4*>(zs + kRows * kLstmB);  // [8][32] float4
   const int tid = threadIdx.x;
+  unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_lstm_trace : nullptr;
+  if (trace) trace += (size_t)4 * a.T1;
   for (int i = tid; i < kRows * HP; i += kLstmThreads) {
     const int r = i / HP, k = i % HP;
     const int gate = r / kLstmU, u = r % kLstmU;
@@ -177,11 +203,28 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(const LstmBwd
   const bool owner = tid < kLstmU * kLstmB && ou < nu && ob < B;
   const int j = u0 + ou;
   const int nq = HP / 4;
+  const int rb = tid % kLstmB, grp = tid / kLstmB;  // reduction role: batch column, CTA group
   float dcf = 0.f;
   __syncthreads();
   for (int t = a.T1 - 1; t >= 0; --t) {
     const size_t trow = (size_t)t * a.ldb + a.b0;
-    float dh_rec = 0.f, ndn = 0.f;
+    if (trace) trace[t * 4 + 0] = gtimer();
+    // the owner's inputs for this step: issued first, consumed after the exchange
+    float dho = 0.f, ig = 0.f, fg = 0.f, gg = 0.f, og = 0.f, c = 0.f, cprev = 0.f, nd = 0.f, ndn = 0.f;
+    if (owner) {
+      const size_t row = trow + ob;
+      dho = a.dh_out[row * a.dh_ld + j];
+      const float* act = a.gates + row * H4;
+      ig = act[j];
+      fg = act[H + j];
+      gg = act[2 * H + j];
+      og = act[3 * H + j];
+      c = a.cseq[row * H + j];
+      nd = a.done[row] ? 0.f : 1.f;
+      cprev = t == 0 ? a.c0[(size_t)(a.b0 + ob) * H + j] : a.cseq[(row - a.ldb) * H + j];
+      if (t + 1 < a.T1) ndn = a.done[row + a.ldb] ? 0.f : 1.f;
+    }
+    float dh_rec = 0.f;
     if (t + 1 < a.T1) {
       float* part = a.part + (size_t)((t + 1) & 1) * G * kLstmB * HP;
       // partial[b][k] = sum over own rows r of dz_{t+1}[r][b] * W_hh[r][k], all k
@@ -209,35 +252,40 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(const LstmBwd
           __stcg(reinterpret_cast<float4*>(mine + (size_t)(bq * 4 + i) * HP + jq * 4),
                  make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]));
       }
+      if (trace) trace[t * 4 + 1] = gtimer();
       grid.sync();
-      {  // fixed-order reduction over CTAs for the own 4 units: thread (b, group)
-        const int b = tid % kLstmB, grp = tid / kLstmB;
-        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int cta = grp; cta < G; cta += 8) {
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)cta * kLstmB + b) * HP + u0));
-          s.x += v.x;
-          s.y += v.y;
-          s.z += v.z;
-          s.w += v.w;
+      if (trace) trace[t * 4 + 2] = gtimer();
+      {  // fixed-order reduction over CTAs for the own 4 units: thread (b, group); all loads
+         // of a thread are issued before the sum (one L2 round trip)
+        constexpr int kMaxPer = (kLstmKmax / kLstmU + 7) / 8;
+        float4 v[kMaxPer];
+#pragma unroll
+        for (int q = 0; q < kMaxPer; ++q) {
+          const int cta = grp + 8 * q;
+          v[q] = cta < G ? __ldcg(reinterpret_cast<const float4*>(part + ((size_t)cta * kLstmB + rb) * HP + u0))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        red[grp * kLstmB + b] = s;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < kMaxPer; ++q) {
+          s.x += v[q].x;
+          s.y += v[q].y;
+          s.z += v[q].z;
+          s.w += v[q].w;
+        }
+        red[grp * kLstmB + rb] = s;
       }
       __syncthreads();
       if (owner) {
 #pragma unroll
-        for (int grp = 0; grp < 8; ++grp) dh_rec += (&red[grp * kLstmB + ob].x)[ou];
-        ndn = a.done[trow + a.ldb + ob] ? 0.f : 1.f;
+        for (int g = 0; g < 8; ++g) dh_rec += (&red[g * kLstmB + ob].x)[ou];
       }
     }
     if (owner) {
       const size_t row = trow + ob;
-      const float dh = a.dh_out[row * a.dh_ld + j] + ndn * dh_rec;
-      const float* act = a.gates + row * H4;
-      const float ig = act[j], fg = act[H + j], gg = act[2 * H + j], og = act[3 * H + j];
-      const float c = a.cseq[row * H + j];
+      const float dh = dho + ndn * dh_rec;
       const float tc = tanhf(c);
-      const float nd = a.done[row] ? 0.f : 1.f;
-      const float cprev = nd * (t == 0 ? a.c0[(size_t)(a.b0 + ob) * H + j] : a.cseq[(row - a.ldb) * H + j]);
+      cprev *= nd;
       const float dc = dh * og * (1.f - tc * tc) + ndn * dcf;
       const float dz[4] = {dc * gg * ig * (1.f - ig), dc * cprev * fg * (1.f - fg), dc * ig * (1.f - gg * gg),
                            dh * tc * og * (1.f - og)};
@@ -250,6 +298,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(const LstmBwd
       }
     }
     __syncthreads();
+    if (trace) trace[t * 4 + 3] = gtimer();
   }
 }
 
@@ -292,6 +341,16 @@ static int check_args(int H, int B, int T1) {
 int lstm_launch_fwd(const LstmFwdArgs& a, cudaStream_t s) {
   if (int e = check_args(a.H, a.B, a.T1)) return e;
   return coop_launch((const void*)lstm_fwd_kernel, a, fwd_smem(a.H), "lstm_fwd_kernel", s);
+}
+
+extern "C" int bp_lstm_trace(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  cudaError_t e = cudaMemcpyToSymbol(g_lstm_trace, &p, sizeof(p));
+  if (e != cudaSuccess) {
+    set_error("lstm trace: %s", cudaGetErrorString(e));
+    return BP_ERR_LAUNCH;
+  }
+  return BP_OK;
 }
 
 int lstm_launch_bwd(const LstmBwdArgs& a, cudaStream_t s) {
