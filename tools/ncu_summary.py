@@ -15,7 +15,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warp_latency_issue_stalled_long_scoreboard", "l1tex__t_bytes.sum",
         "lts__t_sectors_srcunit_tex_op_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 for h, u, v in zip(hdr, units, vals):
-    if h in want or "tensor" in h and "pct" in h and "elapsed" in h:
+    if h in want or h.endswith("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"):
         print(f"{h:70s} {v:>16s} {u}")
 src = list(csv.reader(io.StringIO(page("source", ["--print-source", "sass"]))))
 # find header row

@@ -17,6 +17,6 @@ for k in order:
     tot += t
     rd = float(m.get('dram__bytes_read.sum', '0').replace(',', '')) / 1e6
     wr = float(m.get('dram__bytes_write.sum', '0').replace(',', '')) / 1e6
-    tc = m.get('sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed', '')
+    tc = m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', m.get('sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed', ''))
     print(f"{k:>4} {m['name'][:70]:70s} {m['grid']:>14s} {t/1e3:9.1f} us  rd {rd:8.1f} MB wr {wr:8.1f} MB tc {tc}")
 print("total us", tot / 1e3)
