@@ -226,8 +226,13 @@ typedef struct BpLstmCore {
   float* wpart;   /* [2][G4][576] f32 weight-gradient GEMM outputs           */
 } BpLstmCore;
 size_t bp_lstm_partial_floats(int hidden);
+/* Recurrence implementation: 0 auto (16-CTA cluster kernels with W_hh in registers and
+ * DSMEM exchange when available, else the grid-cooperative kernels), 1 cooperative,
+ * 2 cluster.  Process-wide; for tests and diagnostics. */
+int bp_lstm_set_mode(int mode);
 /* Diagnostics: per-step %globaltimer trace of CTA 0 of the recurrent kernels into
- * buf (device u64 [2][T1][4]: forward phases, then backward phases); NULL disables. */
+ * buf (device u64 [2][T1][4] + 2: forward phases, backward phases, forward start /
+ * end of set-up); NULL disables. */
 int bp_lstm_trace(void* buf);
 /* Forward of T1*B frames through torso + LSTM core + heads.  done [T1*B] u8;
  * h0, c0 [2][B][H] f32 initial state (layer-major, torch (num_layers, B, H));

@@ -44,6 +44,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
     "bp_lstm_partial_floats": (SZ, [I]),
     "bp_lstm_trace": (I, [P]),
+    "bp_lstm_set_mode": (I, [I]),
     "bp_atari_lstm_forward": (I, [P, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),

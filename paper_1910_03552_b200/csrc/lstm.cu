@@ -33,6 +33,8 @@ BP_DEVICE float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
 static __host__ __device__ int lstm_kp(int H) { return (H + 31) & ~31; }
 static __host__ __device__ int lstm_hp(int H) { return (H + 3) & ~3; }
 
+int g_lstm_mode = 0;
+
 int lstm_grid(int H) { return (H + kLstmU - 1) / kLstmU; }
 size_t lstm_part_floats(int H) { return (size_t)2 * lstm_grid(H) * kLstmB * lstm_hp(H); }
 
@@ -343,9 +345,27 @@ int lstm_launch_fwd(const LstmFwdArgs& a, cudaStream_t s) {
   return coop_launch((const void*)lstm_fwd_kernel, a, fwd_smem(a.H), "lstm_fwd_kernel", s);
 }
 
+extern "C" int bp_lstm_set_mode(int mode) {
+  if (mode >= 16) {  // diagnostics: cluster path with debug bits (mode >> 4)
+    g_lstm_mode = mode;
+    return BP_OK;
+  }
+  if (mode < 0 || mode > 2) {
+    set_error("lstm mode %d (0 auto, 1 cooperative, 2 cluster)", mode);
+    return BP_ERR_ARG;
+  }
+  if (mode == 2 && lstm_cluster_batch() == 0) {
+    set_error("lstm: 16-CTA clusters unavailable on this device");
+    return BP_ERR_UNSUPPORTED;
+  }
+  g_lstm_mode = mode;
+  return BP_OK;
+}
+
 extern "C" int bp_lstm_trace(void* buf) {
   unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
   cudaError_t e = cudaMemcpyToSymbol(g_lstm_trace, &p, sizeof(p));
+  if (e == cudaSuccess && lstm_cl_set_trace(buf) != BP_OK) e = cudaErrorUnknown;
   if (e != cudaSuccess) {
     set_error("lstm trace: %s", cudaGetErrorString(e));
     return BP_ERR_LAUNCH;

@@ -27,6 +27,7 @@ struct LstmFwdArgs {
   int aug_ld;
   float* hN;                  // [ldb][H]
   float* cN;                  // [ldb][H]
+  int dbg;                    // diagnostics: bit 0 skip owner global stores, bit 1 skip MMAs
 };
 
 struct LstmBwdArgs {
@@ -44,6 +45,13 @@ struct LstmBwdArgs {
 };
 
 int lstm_grid(int H);
+// cluster path (lstm_cluster.cu): columns per pass (0 = 16-CTA clusters unavailable)
+int lstm_cluster_batch();
+int lstm_cl_launch_fwd(const LstmFwdArgs& a, cudaStream_t s);
+int lstm_cl_launch_bwd(const LstmBwdArgs& a, cudaStream_t s);
+int lstm_cl_set_trace(void* buf);
+// 0 auto (cluster path when available), 1 cooperative grid path, 2 cluster path
+extern int g_lstm_mode;
 int lstm_launch_fwd(const LstmFwdArgs& a, cudaStream_t s);
 int lstm_launch_bwd(const LstmBwdArgs& a, cudaStream_t s);
 size_t lstm_part_floats(int H);

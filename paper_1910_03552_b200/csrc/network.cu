@@ -939,6 +939,12 @@ __global__ void __launch_bounds__(256) lstm_dfc_kernel(const float* __restrict__
 
 extern "C" size_t bp_lstm_partial_floats(int hidden) { return lstm_part_floats(hidden); }
 
+// cluster recurrence when 16-CTA clusters are available (bp_lstm_set_mode overrides)
+static bool lstm_use_cluster() {
+  if ((g_lstm_mode & 15) == 1) return false;
+  return lstm_cluster_batch() > 0;
+}
+
 static int lstm_g4(int H) { return (4 * H + 127) & ~127; }
 
 static int check_lstm(const BpAtariNet* net, const BpLstmCore* core, int T1, int B) {
@@ -991,10 +997,12 @@ extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* co
     g.out = core->gx;
     g.r_img = G4;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
-    for (int b0 = 0; b0 < B; b0 += kLstmB) {
+    const bool cl = lstm_use_cluster();
+    const int pass = cl ? lstm_cluster_batch() : kLstmB;
+    for (int b0 = 0; b0 < B; b0 += pass) {
       LstmFwdArgs a;
       a.H = H;
-      a.B = B - b0 < kLstmB ? B - b0 : kLstmB;
+      a.B = B - b0 < pass ? B - b0 : pass;
       a.ldb = B;
       a.b0 = b0;
       a.T1 = T1;
@@ -1012,7 +1020,8 @@ extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* co
       a.aug_ld = kCoreW;
       a.hN = hN + (size_t)l * B * H;
       a.cN = cN + (size_t)l * B * H;
-      if ((rc = lstm_launch_fwd(a, s))) return rc;
+      a.dbg = g_lstm_mode >> 4;
+      if ((rc = cl ? lstm_cl_launch_fwd(a, s) : lstm_launch_fwd(a, s))) return rc;
     }
   }
   return heads_forward(net, n, bfp(core->out, 1), logits, baseline, s);
@@ -1040,10 +1049,12 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   for (int l = 1; l >= 0; --l) {
     float* dh_in = l == 1 ? core->dh : core->dx;   // gradient w.r.t. this layer's output
     float* dx_out = l == 1 ? core->dx : core->dh;  // gradient w.r.t. this layer's input
-    for (int b0 = 0; b0 < B; b0 += kLstmB) {
+    const bool cl = lstm_use_cluster();
+    const int pass = cl ? lstm_cluster_batch() : kLstmB;
+    for (int b0 = 0; b0 < B; b0 += pass) {
       LstmBwdArgs a;
       a.H = H;
-      a.B = B - b0 < kLstmB ? B - b0 : kLstmB;
+      a.B = B - b0 < pass ? B - b0 : pass;
       a.ldb = B;
       a.b0 = b0;
       a.T1 = T1;
@@ -1057,7 +1068,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       a.part = core->part;
       a.dgates = reinterpret_cast<__nv_bfloat16*>(core->dgates);
       a.dg_ld = G4;
-      if ((rc = lstm_launch_bwd(a, s))) return rc;
+      if ((rc = cl ? lstm_cl_launch_bwd(a, s) : lstm_launch_bwd(a, s))) return rc;
     }
     CUtensorMap ta, tb;
     // weight gradients: D[r][k] = sum_rows dgates[row][r] * X[row][k], X = layer input / previous state

@@ -10,11 +10,13 @@ from paper_1910_03552_b200 import _native as N  # noqa: E402
 from paper_1910_03552_b200.atari_net import AtariNet  # noqa: E402
 
 T1, B, A = 81, 32, 18
+mode = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+N.check(N.lib().bp_lstm_set_mode(mode), "mode")
 dev = torch.device("cuda")
 net = AtariNet(num_actions=A, use_lstm=True)
 batch = make_batch(T1 - 1, B, A, dev, 5)
 n = T1 * B
-tr = torch.zeros(2, T1, 4, dtype=torch.int64, device=dev)
+tr = torch.zeros(2 * T1 * 4 + 2, dtype=torch.int64, device=dev)
 st = net.initial_state(B)
 lstm = dict(T1=T1, B=B, done=batch["done"].reshape(n).view(torch.uint8), h0=st[0], c0=st[1])
 frames = batch["frame"].reshape(n, 4, 84, 84)
@@ -27,10 +29,18 @@ for it in range(3):
                           batch["last_action"].reshape(n), net.flat_grads, lstm=lstm)
     torch.cuda.synchronize()
 N.check(N.lib().bp_lstm_trace(None), "trace off")
-t = tr.cpu().double()
+tall = tr.cpu().double()
+if mode == 2 or mode >= 16:  # cluster kernels record SM cycles: convert at the max SM clock
+    tall = tall / 1.965
+t = tall[:2 * T1 * 4].view(2, T1, 4)
+print("forward set-up us", float(tall[-1] - tall[-2]) / 1e3)
 f = t[0]
-fw = {"copy": f[1:, 1] - f[1:, 0], "compute": f[:, 2] - f[:, 1], "owner": f[:, 3] - f[:, 2],
-      "barrier": f[1:, 0] - f[:-1, 3], "step": f[1:, 0] - f[:-1, 0]}
+if mode == 1:
+    fw = {"copy": f[1:, 1] - f[1:, 0], "compute": f[:, 2] - f[:, 1], "owner": f[:, 3] - f[:, 2],
+          "barrier": f[1:, 0] - f[:-1, 3], "step": f[1:, 0] - f[:-1, 0]}
+else:
+    fw = {"mma": f[:-1, 1] - f[:-1, 0], "owner": f[:-1, 2] - f[:-1, 1], "exchange": f[:-1, 3] - f[:-1, 2],
+          "step": f[1:-1, 0] - f[:-2, 0]}
 print("forward (last layer) ns median:", {k: statistics.median(v.tolist()) for k, v in fw.items()},
       "total us", float(f[-1, 3] - f[0, 0]) / 1e3)
 b = t[1]
