@@ -219,7 +219,9 @@ typedef struct BpLstmCore {
   void* hprev;    /* [2][N][576] bf16 [notdone_t h_{t-1} | 1 | 0], zeroed once */
   void* out;      /* [2][N][576] bf16 [h_t | 1 | 0], zeroed once; out[1] feeds the heads */
   float* hx;      /* [2][H][32] recurrent exchange                           */
-  float* part;    /* bp_lstm_partial_floats(H) backward exchange             */
+  float* part;    /* bp_lstm_partial_floats(H): cooperative-path exchange, or the
+                     cluster path's packed W_hh fragments (written by the forward,
+                     read by the backward of the same step)                */
   void* dgates;   /* [N][G4] bf16 pre-activation gate gradients, zeroed once */
   float* dh;      /* [N][576] f32                                            */
   float* dx;      /* [N][576] f32                                            */

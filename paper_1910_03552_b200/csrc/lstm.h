@@ -28,6 +28,7 @@ struct LstmFwdArgs {
   float* hN;                  // [ldb][H]
   float* cN;                  // [ldb][H]
   int dbg;                    // diagnostics: bit 0 skip owner global stores, bit 1 skip MMAs
+  const uint32_t* wfrag;      // cluster path: packed forward A-fragments (lstm_cl_pack)
 };
 
 struct LstmBwdArgs {
@@ -42,6 +43,7 @@ struct LstmBwdArgs {
   float* part;                // [2][grid][kLstmB][Hp] recurrent partial sums
   __nv_bfloat16* dgates;      // [rows][dg_ld] pre-activation gate gradients
   int dg_ld;
+  const uint32_t* wfrag;      // cluster path: packed backward A-fragments (lstm_cl_pack)
 };
 
 int lstm_grid(int H);
@@ -50,6 +52,10 @@ int lstm_cluster_batch();
 int lstm_cl_launch_fwd(const LstmFwdArgs& a, cudaStream_t s);
 int lstm_cl_launch_bwd(const LstmBwdArgs& a, cudaStream_t s);
 int lstm_cl_set_trace(void* buf);
+// W_hh -> packed bf16 A-fragments of both cluster kernels (forward block, then backward)
+size_t lstm_cl_frag_words();
+size_t lstm_cl_frag_dir_words();
+int lstm_cl_pack(const float* whh, int H, uint32_t* frag, cudaStream_t s);
 // 0 auto (cluster path when available), 1 cooperative grid path, 2 cluster path
 extern int g_lstm_mode;
 int lstm_launch_fwd(const LstmFwdArgs& a, cudaStream_t s);

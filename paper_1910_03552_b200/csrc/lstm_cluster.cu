@@ -154,25 +154,17 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
   unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_cl_trace : nullptr;
   if (trace) trace[4 * a.T1 * 2] = gtimer();
 
-  // ---- A fragments of this warp's items: rows mt*16.., K-steps of quarter kq
+  // ---- A fragments of this warp's items (rows mt*16.., K-steps of quarter kq), pre-packed
+  //      by lstm_cl_pack in per-lane order: coalesced 4-byte loads
   uint32_t af[ITEMS][KSMAX][4];
+  {
+    const uint32_t* fp = a.wfrag + (size_t)(rank * WARPS + warp) * (ITEMS * KSMAX * 4 * 32) + lane;
 #pragma unroll
-  for (int s = 0; s < ITEMS; ++s) {
-    const int item = warp + WARPS * s;  // 0..35
-    const int mt = item % MT, kq = item / MT;
+    for (int s = 0; s < ITEMS; ++s)
 #pragma unroll
-    for (int q = 0; q < KSMAX; ++q) {
-      const int ks = kq * 9 + q;
-      const int r0 = mt * 16 + g, c0 = ks * 16 + 2 * tig;
-      if (ks < KST) {
-        af[s][q][0] = pack2(w_local(a.whh, H, rank, r0, c0), w_local(a.whh, H, rank, r0, c0 + 1));
-        af[s][q][1] = pack2(w_local(a.whh, H, rank, r0 + 8, c0), w_local(a.whh, H, rank, r0 + 8, c0 + 1));
-        af[s][q][2] = pack2(w_local(a.whh, H, rank, r0, c0 + 8), w_local(a.whh, H, rank, r0, c0 + 9));
-        af[s][q][3] = pack2(w_local(a.whh, H, rank, r0 + 8, c0 + 8), w_local(a.whh, H, rank, r0 + 8, c0 + 9));
-      } else {
-        af[s][q][0] = af[s][q][1] = af[s][q][2] = af[s][q][3] = 0u;
-      }
-    }
+      for (int q = 0; q < KSMAX; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) af[s][q][r] = __ldg(fp + ((s * KSMAX + q) * 4 + r) * 32);
   }
   // ---- h0 of this cluster's columns (all units); padding zero
   for (int i = tid; i < NB * KPS; i += THREADS) {
@@ -342,23 +334,16 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
   const int u0 = rank * UC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tig = lane & 3;
 
-  // ---- A fragments of W_hh^T: rows = hidden column j (34 tiles of 16), K = own gate rows (9 steps)
+  // ---- A fragments of W_hh^T (rows = hidden column j, K = own gate rows), pre-packed
   uint32_t af[ITEMS][KSMAX][4];
+  {
+    const uint32_t* fp = a.wfrag + (size_t)(rank * WARPS + warp) * (ITEMS * KSMAX * 4 * 32) + lane;
 #pragma unroll
-  for (int s = 0; s < ITEMS; ++s) {
-    const int mt = warp + WARPS * s;  // 0..35; tiles >= 34 are empty
+    for (int s = 0; s < ITEMS; ++s)
 #pragma unroll
-    for (int q = 0; q < KSMAX; ++q) {
-      const int j0 = mt * 16 + g, r0 = q * 16 + 2 * tig;
-      if (mt < KST) {
-        af[s][q][0] = pack2(w_local(a.whh, H, rank, r0, j0), w_local(a.whh, H, rank, r0 + 1, j0));
-        af[s][q][1] = pack2(w_local(a.whh, H, rank, r0, j0 + 8), w_local(a.whh, H, rank, r0 + 1, j0 + 8));
-        af[s][q][2] = pack2(w_local(a.whh, H, rank, r0 + 8, j0), w_local(a.whh, H, rank, r0 + 9, j0));
-        af[s][q][3] = pack2(w_local(a.whh, H, rank, r0 + 8, j0 + 8), w_local(a.whh, H, rank, r0 + 9, j0 + 8));
-      } else {
-        af[s][q][0] = af[s][q][1] = af[s][q][2] = af[s][q][3] = 0u;
-      }
-    }
+      for (int q = 0; q < KSMAX; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) af[s][q][r] = __ldg(fp + ((s * KSMAX + q) * 4 + r) * 32);
   }
   unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_cl_trace : nullptr;
   if (trace) trace += (size_t)4 * a.T1;
@@ -474,6 +459,53 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
   }
   if (tid < CS) bulk_wait_read_all();
   cluster_sync_all();
+}
+
+// --------------------------------------------------------------------------- fragment pack
+// W_hh (f32, torch layout) -> per-lane bf16 mma.sync A-fragments of both recurrent kernels:
+// frag[dir][rank][warp][item][kstep][reg][lane] (u32 = 2 bf16), dir 0 forward (rows = own
+// gate rows, K = hidden), dir 1 backward (rows = hidden, K = own gate rows).  Run once per
+// weight update; the kernels then load their ~108 fragment registers with coalesced loads.
+__global__ void lstm_cl_pack_kernel(const float* __restrict__ whh, int H, uint32_t* __restrict__ frag) {
+  constexpr int PER_WARP = ITEMS * KSMAX * 4 * 32;
+  constexpr int PER_DIR = CS * WARPS * PER_WARP;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * PER_DIR; i += gridDim.x * blockDim.x) {
+    const int dir = i / PER_DIR;
+    int rem = i % PER_DIR;
+    const int rank = rem / (WARPS * PER_WARP);
+    rem %= WARPS * PER_WARP;
+    const int warp = rem / PER_WARP;
+    rem %= PER_WARP;
+    const int s = rem / (KSMAX * 128), q = (rem / 128) % KSMAX, r = (rem / 32) % 4, lane = rem % 32;
+    const int g = lane >> 2, tig = lane & 3;
+    float v0 = 0.f, v1 = 0.f;
+    if (dir == 0) {
+      const int item = warp + WARPS * s;
+      const int mt = item % MT, kq = item / MT;
+      const int ks = kq * 9 + q;
+      if (ks < KST) {
+        const int row = mt * 16 + g + ((r & 1) ? 8 : 0), c0 = ks * 16 + 2 * tig + ((r & 2) ? 8 : 0);
+        v0 = w_local(whh, H, rank, row, c0);
+        v1 = w_local(whh, H, rank, row, c0 + 1);
+      }
+    } else {
+      const int mt = warp + WARPS * s;
+      if (mt < KST) {
+        const int jrow = mt * 16 + g + ((r & 1) ? 8 : 0), k0 = q * 16 + 2 * tig + ((r & 2) ? 8 : 0);
+        v0 = w_local(whh, H, rank, k0, jrow);
+        v1 = w_local(whh, H, rank, k0 + 1, jrow);
+      }
+    }
+    frag[i] = pack2(v0, v1);
+  }
+}
+
+size_t lstm_cl_frag_words() { return (size_t)2 * CS * WARPS * ITEMS * KSMAX * 4 * 32; }
+size_t lstm_cl_frag_dir_words() { return (size_t)CS * WARPS * ITEMS * KSMAX * 4 * 32; }
+
+int lstm_cl_pack(const float* whh, int H, uint32_t* frag, cudaStream_t s) {
+  lstm_cl_pack_kernel<<<296, 256, 0, s>>>(whh, H, frag);
+  return check_launch("lstm_cl_pack_kernel");
 }
 
 // --------------------------------------------------------------------------- launch

@@ -937,7 +937,11 @@ __global__ void __launch_bounds__(256) lstm_dfc_kernel(const float* __restrict__
   }
 }
 
-extern "C" size_t bp_lstm_partial_floats(int hidden) { return lstm_part_floats(hidden); }
+// cooperative path: recurrent partial sums; cluster path: packed W_hh fragments of both layers
+extern "C" size_t bp_lstm_partial_floats(int hidden) {
+  const size_t coop = lstm_part_floats(hidden), cl = 2 * lstm_cl_frag_words();
+  return coop > cl ? coop : cl;
+}
 
 // cluster recurrence when 16-CTA clusters are available (bp_lstm_set_mode overrides)
 static bool lstm_use_cluster() {
@@ -999,6 +1003,9 @@ extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* co
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
     const bool cl = lstm_use_cluster();
     const int pass = cl ? lstm_cluster_batch() : kLstmB;
+    if (cl && (rc = lstm_cl_pack(params + off[l ? P_WHH1 : P_WHH0], H,
+                                 reinterpret_cast<uint32_t*>(core->part) + (size_t)l * lstm_cl_frag_words(), s)))
+      return rc;
     for (int b0 = 0; b0 < B; b0 += pass) {
       LstmFwdArgs a;
       a.H = H;
@@ -1021,6 +1028,7 @@ extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* co
       a.hN = hN + (size_t)l * B * H;
       a.cN = cN + (size_t)l * B * H;
       a.dbg = g_lstm_mode >> 4;
+      a.wfrag = reinterpret_cast<const uint32_t*>(core->part) + (size_t)l * lstm_cl_frag_words();
       if ((rc = cl ? lstm_cl_launch_fwd(a, s) : lstm_launch_fwd(a, s))) return rc;
     }
   }
@@ -1068,6 +1076,8 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       a.part = core->part;
       a.dgates = reinterpret_cast<__nv_bfloat16*>(core->dgates);
       a.dg_ld = G4;
+      a.wfrag = reinterpret_cast<const uint32_t*>(core->part) + (size_t)l * lstm_cl_frag_words() +
+                lstm_cl_frag_dir_words();
       if ((rc = cl ? lstm_cl_launch_bwd(a, s) : lstm_launch_bwd(a, s))) return rc;
     }
     CUtensorMap ta, tb;
