@@ -195,6 +195,16 @@ int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stre
 int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
                      const int64_t* last_action, const float* params, float* logits,
                      float* baseline, void* stream);
+/* Forward with frame-stack dedup: the frames are not shipped as [n][4][84][84]
+ * but as a plane store planes u8 [num_planes][84][84] (one plane per env step) and
+ * plane_index int32 [n][4]: channel c of frame i is planes[plane_index[i*4 + c]]
+ * (indices are clamped to [0, num_planes)).  Results are bit-identical to bp_atari_forward
+ * on the stacked frames.  Replaces the np.stack of stacked frames at enqueue
+ * (rollout.py:116-144); upstream FrameStack semantics are built by
+ * rollout.frame_stack_index. */
+int bp_atari_forward_planes(const BpAtariNet* net, int n, const uint8_t* planes, const int32_t* plane_index,
+                            int num_planes, const float* reward, const int64_t* last_action,
+                            const float* params, float* logits, float* baseline, void* stream);
 /* Backward of the last forward: d_logits [n][A], d_baseline [n] -> grads (flat f32,
  * same layout as params; every entry is overwritten). */
 int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
@@ -243,6 +253,12 @@ int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1,
                           const uint8_t* frames, const float* reward, const int64_t* last_action,
                           const uint8_t* done, const float* params, const float* h0, const float* c0,
                           float* logits, float* baseline, float* hN, float* cN, void* stream);
+/* bp_atari_lstm_forward on a deduplicated plane store (see bp_atari_forward_planes). */
+int bp_atari_lstm_forward_planes(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                 const uint8_t* planes, const int32_t* plane_index, int num_planes,
+                                 const float* reward, const int64_t* last_action, const uint8_t* done,
+                                 const float* params, const float* h0, const float* c0, float* logits,
+                                 float* baseline, float* hN, float* cN, void* stream);
 /* Backward of the last bp_atari_lstm_forward (same T1, B, done, c0): d_logits [N][A],
  * d_baseline [N] -> grads (flat, every entry overwritten).  The initial state gets no
  * gradient (upstream learn() feeds the actors' state as a constant). */

@@ -41,11 +41,13 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_workspace_bytes": (SZ, [I, I]),
     "bp_atari_pack_weights": (I, [P, P, P]),
     "bp_atari_forward": (I, [P, I, P, P, P, P, P, P, P]),
+    "bp_atari_forward_planes": (I, [P, I, P, P, I, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
     "bp_lstm_partial_floats": (SZ, [I]),
     "bp_lstm_trace": (I, [P]),
     "bp_lstm_set_mode": (I, [I]),
     "bp_atari_lstm_forward": (I, [P, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "bp_atari_lstm_forward_planes": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),

@@ -272,14 +272,26 @@ class AtariNet(nn.Module):
                 getattr(self, "_packed_version", None) != self.flat_params._version)
 
     def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
-                         repack: bool | None = None, lstm: dict | None = None):
+                         repack: bool | None = None, lstm: dict | None = None, plane_index=None):
         """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
 
+        Frame-stack dedup: with plane_index (n,4) int32, `frames` is a plane store
+        (P,84,84) u8 and channel c of frame i is frames[plane_index[i, c]]
+        (rollout.frame_stack_index builds the upstream FrameStack indexing).
         repack=None packs the bf16 mirror only when stale; False trusts it (the fused
         optimiser step keeps it fresh); True always packs.  LSTM nets take
         lstm=dict(T1, B, done u8 (n,), h0, c0 (2,B,H) f32[, hN, cN]); the final state
         is returned in lstm["hN"], lstm["cN"]."""
-        n = frames.shape[0]
+        if plane_index is not None:
+            if plane_index.dtype != torch.int32 or plane_index.shape[-1] != 4:
+                raise DimensionError("plane_index must be int32 (n, 4)")
+            if frames.dim() < 3 or tuple(frames.shape[-2:]) != OBS_SHAPE[1:]:
+                raise DimensionError(f"plane store must be (..., 84, 84), got {tuple(frames.shape)}")
+            frames = frames.reshape(-1, *OBS_SHAPE[1:])
+            plane_index = plane_index.reshape(-1, 4)
+            n, num_planes = plane_index.shape[0], frames.shape[0]
+        else:
+            n = frames.shape[0]
         b = self.buffers_for(n)
         if repack or (repack is None and self.mirror_stale()):
             self.pack_weights()
@@ -298,15 +310,24 @@ class AtariNet(nn.Module):
             for k in ("hN", "cN"):
                 if lstm.get(k) is None:
                     lstm[k] = torch.empty(shape, device=frames.device)
-            N.check(N.lib().bp_atari_lstm_forward(
-                b.ref, b.lstm.ref, T1, B, N.ptr(frames), N.ptr(reward), N.ptr(last_action),
-                N.ptr(lstm["done"]), N.ptr(self.flat_params), N.ptr(lstm["h0"]), N.ptr(lstm["c0"]),
-                N.ptr(logits), N.ptr(baseline), N.ptr(lstm["hN"]), N.ptr(lstm["cN"]), stream),
-                "bp_atari_lstm_forward")
+            tail = (N.ptr(reward), N.ptr(last_action), N.ptr(lstm["done"]), N.ptr(self.flat_params),
+                    N.ptr(lstm["h0"]), N.ptr(lstm["c0"]), N.ptr(logits), N.ptr(baseline),
+                    N.ptr(lstm["hN"]), N.ptr(lstm["cN"]), stream)
+            if plane_index is not None:
+                N.check(N.lib().bp_atari_lstm_forward_planes(
+                    b.ref, b.lstm.ref, T1, B, N.ptr(frames), N.ptr(plane_index), num_planes, *tail),
+                    "bp_atari_lstm_forward_planes")
+            else:
+                N.check(N.lib().bp_atari_lstm_forward(b.ref, b.lstm.ref, T1, B, N.ptr(frames), *tail),
+                        "bp_atari_lstm_forward")
         else:
-            N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), N.ptr(reward), N.ptr(last_action),
-                                             N.ptr(self.flat_params), N.ptr(logits), N.ptr(baseline),
-                                             stream), "bp_atari_forward")
+            tail = (N.ptr(reward), N.ptr(last_action), N.ptr(self.flat_params), N.ptr(logits),
+                    N.ptr(baseline), stream)
+            if plane_index is not None:
+                N.check(N.lib().bp_atari_forward_planes(b.ref, n, N.ptr(frames), N.ptr(plane_index),
+                                                        num_planes, *tail), "bp_atari_forward_planes")
+            else:
+                N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), *tail), "bp_atari_forward")
         self._last_n = n
         return logits, baseline
 

@@ -128,9 +128,13 @@ static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorM
 constexpr int kCoreW = 576;  // augmented core row: 512 fc + clip(r) + onehot(A) + 1 + zero pad
 
 // u8 frames [N,4,84,84] -> X0 [N*21*21, 64] bf16, channel = ci*16 + ry*4 + rx.
+// Frame-stack dedup (plane_index != null): `frames` is a plane store [P][84][84] and channel
+// ci of frame img is plane plane_index[img*4 + ci] (clamped to [0, num_planes)).
 // The Y == 0 CTA of each image also writes the augmented core columns 512..575:
 // [clip(reward), onehot(last_action) (A), 1 (bias), 0 ...]  (core order of upstream AtariNet).
 __global__ void __launch_bounds__(128) frames_s2d_kernel(const uint8_t* __restrict__ frames,
+                                                         const int32_t* __restrict__ plane_index,
+                                                         int num_planes,
                                                          __nv_bfloat16* __restrict__ x0,
                                                          const float* __restrict__ reward,
                                                          const int64_t* __restrict__ last_action,
@@ -148,8 +152,13 @@ __global__ void __launch_bounds__(128) frames_s2d_kernel(const uint8_t* __restri
   for (int w = threadIdx.x; w < 16 * 21; w += 128) {
     const int row = w / 21, col = w % 21;  // row = ci*4 + ry
     const int ci = row >> 2, ry = row & 3;
+    size_t plane = (size_t)img * 4 + ci;
+    if (plane_index) {
+      const int pi = __ldg(plane_index + plane);
+      plane = (size_t)(pi < 0 ? 0 : pi >= num_planes ? num_planes - 1 : pi);
+    }
     const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(
-        frames + (((size_t)img * 4 + ci) * 84 + (4 * Y + ry)) * 84) + col);
+        frames + (plane * 84 + (4 * Y + ry)) * 84) + col);
     *reinterpret_cast<uint32_t*>(&slab[ci][ry][4 * col]) = v;
   }
   __syncthreads();
@@ -514,15 +523,17 @@ extern "C" int bp_atari_pack_weights(const BpAtariNet* net, const float* params,
 }
 
 // frames -> conv torso -> fc -> augmented core [n][576] (net->core)
-static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
-                         const int64_t* last_action, const float* params, const int64_t* off,
-                         cudaStream_t s) {
+// frames: u8 [n][4][84][84], or (plane_index != null) a plane store [num_planes][84][84]
+static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
+                         int num_planes, const float* reward, const int64_t* last_action,
+                         const float* params, const int64_t* off, cudaStream_t s) {
   const int A = net->num_actions;
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
-  frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, bf(net->x0), reward, last_action, bf(net->core), A);
+  frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
+                                           bf(net->core), A);
   if ((rc = check_launch("frames_s2d_kernel"))) return rc;
   pack_heads_kernel<<<36, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
                                        params + off[P_BV], bf(net->whf), A);
@@ -638,10 +649,19 @@ static int heads_forward(const BpAtariNet* net, int n, const void* head_in, floa
   return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s);
 }
 
-extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
-                                const float* reward, const int64_t* last_action, const float* params,
-                                float* logits, float* baseline, void* stream) {
+static int check_planes(const uint8_t* planes, const int32_t* plane_index, int num_planes) {
+  if (!planes || (plane_index && num_planes < 1)) {
+    set_error("atari: null frames / plane store, or num_planes < 1");
+    return BP_ERR_ARG;
+  }
+  return BP_OK;
+}
+
+static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
+                         int num_planes, const float* reward, const int64_t* last_action, const float* params,
+                         float* logits, float* baseline, void* stream) {
   if (int e = check_net(net, n)) return e;
+  if (int e = check_planes(frames, plane_index, num_planes)) return e;
   if (net->use_lstm) {
     set_error("atari: LSTM net -> bp_atari_lstm_forward");
     return BP_ERR_ARG;
@@ -650,8 +670,27 @@ extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* fra
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 0, off);
   int rc;
-  if ((rc = torso_forward(net, n, frames, reward, last_action, params, off, s))) return rc;
+  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
+    return rc;
   return heads_forward(net, n, net->core, logits, baseline, s);
+}
+
+extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
+                                const float* reward, const int64_t* last_action, const float* params,
+                                float* logits, float* baseline, void* stream) {
+  return atari_forward(net, n, frames, nullptr, 0, reward, last_action, params, logits, baseline, stream);
+}
+
+extern "C" int bp_atari_forward_planes(const BpAtariNet* net, int n, const uint8_t* planes,
+                                       const int32_t* plane_index, int num_planes, const float* reward,
+                                       const int64_t* last_action, const float* params, float* logits,
+                                       float* baseline, void* stream) {
+  if (!plane_index) {
+    set_error("atari: bp_atari_forward_planes needs a plane index");
+    return BP_ERR_ARG;
+  }
+  return atari_forward(net, n, planes, plane_index, num_planes, reward, last_action, params, logits, baseline,
+                       stream);
 }
 
 // G = [d_logits | d_baseline | 0] bf16, then the heads data-gradient:
@@ -961,18 +1000,20 @@ static int check_lstm(const BpAtariNet* net, const BpLstmCore* core, int T1, int
   return BP_OK;
 }
 
-extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
-                                     const uint8_t* frames, const float* reward, const int64_t* last_action,
-                                     const uint8_t* done, const float* params, const float* h0,
-                                     const float* c0, float* logits, float* baseline, float* hN, float* cN,
-                                     void* stream) {
+static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                              const uint8_t* frames, const int32_t* plane_index, int num_planes,
+                              const float* reward, const int64_t* last_action, const uint8_t* done,
+                              const float* params, const float* h0, const float* c0, float* logits,
+                              float* baseline, float* hN, float* cN, void* stream) {
   if (int e = check_lstm(net, core, T1, B)) return e;
+  if (int e = check_planes(frames, plane_index, num_planes)) return e;
   cudaStream_t s = (cudaStream_t)stream;
   const int n = T1 * B, H = core->hidden, G4 = lstm_g4(H);
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 1, off);
   int rc;
-  if ((rc = torso_forward(net, n, frames, reward, last_action, params, off, s))) return rc;
+  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
+    return rc;
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(core->wih);
   const size_t wsz = (size_t)G4 * kCoreW;
   for (int l = 0; l < 2; ++l) {
@@ -1033,6 +1074,29 @@ extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* co
     }
   }
   return heads_forward(net, n, bfp(core->out, 1), logits, baseline, s);
+}
+
+extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                     const uint8_t* frames, const float* reward, const int64_t* last_action,
+                                     const uint8_t* done, const float* params, const float* h0,
+                                     const float* c0, float* logits, float* baseline, float* hN, float* cN,
+                                     void* stream) {
+  return atari_lstm_forward(net, core, T1, B, frames, nullptr, 0, reward, last_action, done, params, h0, c0,
+                            logits, baseline, hN, cN, stream);
+}
+
+extern "C" int bp_atari_lstm_forward_planes(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                            const uint8_t* planes, const int32_t* plane_index, int num_planes,
+                                            const float* reward, const int64_t* last_action,
+                                            const uint8_t* done, const float* params, const float* h0,
+                                            const float* c0, float* logits, float* baseline, float* hN,
+                                            float* cN, void* stream) {
+  if (!plane_index) {
+    set_error("atari: bp_atari_lstm_forward_planes needs a plane index");
+    return BP_ERR_ARG;
+  }
+  return atari_lstm_forward(net, core, T1, B, planes, plane_index, num_planes, reward, last_action, done, params,
+                            h0, c0, logits, baseline, hN, cN, stream);
 }
 
 extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
