@@ -416,7 +416,8 @@ def main():
     e1.synchronize()
     h2d_gbs = 5 * h2d_full / (e0.elapsed_time(e1) * 1e-3) / 1e9
     del hbuf, dbuf
-    learner.learn(FLAGS, None, model, batch, (), opt, None, process_group=pg)
+    for _ in range(3):  # eager, graph capture, replay
+        learner.learn(FLAGS, None, model, batch, (), opt, None, process_group=pg)
     torch.cuda.synchronize()
     e0.record(s)
     for _ in range(n_e2e):

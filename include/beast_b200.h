@@ -195,6 +195,14 @@ int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stre
 int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
                      const int64_t* last_action, const float* params, float* logits,
                      float* baseline, void* stream);
+/* Debug: the next tcgen05 GEMM launch records per-tile role timestamps (%globaltimer, ns)
+ * into buf[(cta * tiles + i) * 16 + event]: 0/1 producer, 2/3 MMA, 4/5 epilogue, 6/7 u8
+ * converter (start / end of tile i of that CTA), 8/9 converter loop end / fence end.  buf = null cancels. */
+int bp_gemm_trace_next(void* buf, int tiles);
+/* conv1 operand path: 1 (default) builds the conv1 A operand on chip from the u8 frames
+ * (no bf16 space-to-depth grid in HBM); 0 uses the bf16 X0 grid.  Results are identical.
+ * on < 0 only queries.  Returns the previous setting.  (Test / A-B knob, process-global.) */
+int bp_atari_set_conv1_u8(int on);
 /* Forward with frame-stack dedup: the frames are not shipped as [n][4][84][84]
  * but as a plane store planes u8 [num_planes][84][84] (one plane per env step) and
  * plane_index int32 [n][4]: channel c of frame i is planes[plane_index[i*4 + c]]

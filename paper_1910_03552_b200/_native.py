@@ -41,6 +41,8 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_workspace_bytes": (SZ, [I, I]),
     "bp_atari_pack_weights": (I, [P, P, P]),
     "bp_atari_forward": (I, [P, I, P, P, P, P, P, P, P]),
+    "bp_atari_set_conv1_u8": (I, [I]),
+    "bp_gemm_trace_next": (I, [P, I]),
     "bp_atari_forward_planes": (I, [P, I, P, P, I, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
     "bp_lstm_partial_floats": (SZ, [I]),

@@ -28,6 +28,7 @@
 // augmented core [relu(fc) | clip(r) | onehot(a) | 1].
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -70,6 +71,17 @@ static int make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long 
 }
 
 // window mode for a shifted K-major A operand: taps share one TMA box per channel block
+// conv1 A operand straight from the u8 frames (BP_CONV1_U8=0 or bp_atari_set_conv1_u8(0) restore
+// the bf16 X0 grid path: space-to-depth kernel + TMA-loaded windows)
+static int g_conv1_u8 = -1;
+static bool conv1_u8() {
+  if (g_conv1_u8 < 0) {
+    const char* e = std::getenv("BP_CONV1_U8");
+    g_conv1_u8 = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_conv1_u8 != 0;
+}
+
 static void set_window(GemmArgs& g, int taps) {
   int mn = 0, mx = 0;
   for (int t = 0; t < taps; ++t) {
@@ -96,10 +108,20 @@ static GemmArgs base_args() {
   return g;
 }
 
-template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0>
-static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, AM, BM, BSWZ, BRES, AW>;
-  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW>;
+static void* g_trace_next = nullptr;
+static int g_trace_tiles = 0;
+
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
+static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
+  GemmArgs g = g0;
+  gemm_prepare(g);
+  if (g_trace_next) {  // debug: per-tile role timeline of this launch (bp_gemm_trace_next)
+    g.trace = reinterpret_cast<unsigned long long*>(g_trace_next);
+    g.trace_tiles = g_trace_tiles;
+    g_trace_next = nullptr;
+  }
+  using Cfg = GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>;
+  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW, AU8>;
   if (AW && (g.a_win_rows > 160 || g.a_win_rows < 128 || g.a_ntaps < 1 || g.a_ntaps > kMaxShifts)) {
     set_error("gemm: window rows %d / taps %d unsupported", g.a_win_rows, g.a_ntaps);
     return BP_ERR_ARG;
@@ -119,7 +141,7 @@ static int launch_gemm(const GemmArgs& g, const CUtensorMap& ta, const CUtensorM
   }
   const int tiles = g.m_tiles * g.n_tiles * g.splits;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  kern<<<grid, kGemmThreads, Cfg::SMEM, s>>>(g, ta, tb);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, ta, tb);
   return check_launch("umma_gemm_kernel");
 }
 
@@ -176,6 +198,21 @@ __global__ void __launch_bounds__(128) frames_s2d_kernel(const uint8_t* __restri
     }
     *reinterpret_cast<uint4*>(dst + (size_t)X * 64 + ch0) = make_uint4(w[0], w[1], w[2], w[3]);
   }
+}
+
+// Augmented core columns 512..575 of every frame: [clip(reward), onehot(last_action) (A),
+// 1 (bias), 0 ...] (the frames_s2d_kernel side job, for the u8 conv1 path)
+__global__ void core_aug_kernel(const float* __restrict__ reward, const int64_t* __restrict__ last_action,
+                                __nv_bfloat16* __restrict__ core, int n, int A) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * 64) return;
+  const long long img = i >> 6;
+  const int j = (int)(i & 63);
+  float v = 0.f;
+  if (j == 0) v = fminf(fmaxf(reward[img], -1.f), 1.f);
+  else if (j <= A) v = (last_action[img] == j - 1) ? 1.f : 0.f;
+  else if (j == A + 1) v = 1.f;
+  core[img * kCoreW + 512 + j] = __float2bfloat16_rn(v);
 }
 
 // G [N][64] bf16 = [d_logits (A) | d_baseline | 0 ...]
@@ -481,6 +518,20 @@ extern "C" int bp_gemm_shift_test(const void* A, const void* B, float* Cout, int
   return launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 2>(g, ta, tb, s);
 }
 
+// debug: the next GEMM launch records per-tile role timestamps (%globaltimer ns) into
+// buf[(cta * tiles + i) * 16 + event] (0/1 producer, 2/3 MMA, 4/5 epilogue, 6/7 u8 converter)
+extern "C" int bp_gemm_trace_next(void* buf, int tiles) {
+  g_trace_next = buf;
+  g_trace_tiles = tiles;
+  return BP_OK;
+}
+
+extern "C" int bp_atari_set_conv1_u8(int on) {
+  const int prev = conv1_u8() ? 1 : 0;
+  if (on >= 0) g_conv1_u8 = on ? 1 : 0;
+  return prev;
+}
+
 extern "C" int64_t bp_atari_param_count(int num_actions, int use_lstm) {
   if (num_actions < 1 || num_actions > 31) return -1;
   int64_t off[P_COUNT + 1];
@@ -532,14 +583,20 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
-  frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
-                                           bf(net->core), A);
-  if ((rc = check_launch("frames_s2d_kernel"))) return rc;
+  if (conv1_u8()) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
+    core_aug_kernel<<<(n * 64 + 255) / 256, 256, 0, s>>>(reward, last_action, bf(net->core), n, A);
+    if ((rc = check_launch("core_aug_kernel"))) return rc;
+  } else {
+    frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
+                                             bf(net->core), A);
+    if ((rc = check_launch("frames_s2d_kernel"))) return rc;
+  }
   pack_heads_kernel<<<36, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
                                        params + off[P_BV], bf(net->whf), A);
   if ((rc = check_launch("pack_heads_kernel"))) return rc;
   CUtensorMap ta, tb;
   // 2. conv1: X0 [n*441, 64] x W1 [32, 256] -> relu(./255 + b1) -> X1 (s2d-2 layout)
+  //    u8 mode: the X0 window of every tile is built on chip from the u8 frames
   {
     const long long R = (long long)n * 441;
     GemmArgs g = base_args();
@@ -549,8 +606,17 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     const int offs[4] = {0, 1, 21, 22};
     for (int i = 0; i < 4; ++i) g.a_row_off[i] = offs[i];
     set_window(g, 4);
-    if ((rc = make_tmap(&ta, net->x0, R, 64, 64, g.a_win_rows, 128))) return rc;
     if ((rc = make_tmap(&tb, wbf + off[P_W1], 32, 256, 64, 32, 128))) return rc;
+    if (conv1_u8()) {
+      ta = tb;  // (unused by the u8 producer)
+      g.u8 = frames;
+      g.u8_index = plane_index;
+      g.u8_planes = num_planes;
+      g.u8_rows = R;
+      g.u8_x0_out = bf(net->x0);
+    } else if ((rc = make_tmap(&ta, net->x0, R, 64, 64, g.a_win_rows, 128))) {
+      return rc;
+    }
     g.N = 32;
     g.M = (int)R;
     g.alpha = 1.f / 255.f;
@@ -560,7 +626,11 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.bits_out = reinterpret_cast<uint32_t*>(net->m1);
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
-    if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
+    if (conv1_u8()) {
+      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 1>(g, ta, tb, s))) return rc;
+    } else if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) {
+      return rc;
+    }
   }
   // 3. conv2: X1 [n*100, 128], 2x2 taps on the 10x10 grid -> X2 [n*81, 64]
   {

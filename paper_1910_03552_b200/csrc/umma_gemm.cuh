@@ -27,6 +27,18 @@ constexpr int kMaxShifts = 16;
 enum AMode { A_KMAJOR = 0, A_MNMAJOR = 1 };
 enum BMode { B_KMAJOR = 0, B_MNMAJOR = 1 };
 
+// n / d for n < 2^31 by a precomputed multiplier (round-up method): q = (umulhi(n, mul) + n) >> shift
+struct FDiv {
+  uint32_t mul, shift;
+};
+inline FDiv fdiv_make(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  const unsigned long long m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+  return FDiv{(uint32_t)m, l};
+}
+BP_DEVICE uint32_t fdivu(uint32_t n, FDiv f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+
 struct GemmArgs {
   // tiling
   int m_tiles, n_tiles, splits;
@@ -66,14 +78,35 @@ struct GemmArgs {
   // bias-gradient column sums of the stored (post-mask) values, deterministic:
   // colsum[(mt * 4 + epilogue_warp) * N + n] = sum over that warp's 32 rows (splits == 1)
   float* colsum;
-  // optional per-tile timeline (test builds): trace[(blockIdx.x * trace_tiles + i) * 8 + event]
+  // optional per-tile timeline (test builds): trace[(blockIdx.x * trace_tiles + i) * 16 + event]
   unsigned long long* trace;
   int trace_tiles;
   // AtariNet heads epilogue (heads != 0): column j < A -> logits[m][j], j == A -> baseline[m]
   int heads, A;
   float* logits;   // [M][A] f32
   float* baseline; // [M] f32
+  // AU8 (conv1): the A operand is built on chip from u8 frames instead of a bf16 grid.
+  // Grid row r = img*441 + gy*21 + gx, channel ci*16 + ry*4 + rx of row r is
+  // frame(img, ci)[4gy + ry][4gx + rx]; frame(img, ci) = u8 + plane * 7056 with
+  // plane = u8_index ? clamp(u8_index[img*4 + ci], 0, u8_planes - 1) : img*4 + ci.
+  const uint8_t* u8;
+  const int32_t* u8_index;
+  int u8_planes;
+  long long u8_rows;  // valid grid rows (n * 441); rows beyond convert to zero
+  __nv_bfloat16* u8_x0_out;  // optional: the converted grid rows of every tile also go to HBM
+                             // as X0 [rows][64] bf16 (the conv1 weight-gradient operand)
+  // epilogue divisors (filled by the launcher from gh*gw, gw, sy, sx, cdiv, cq)
+  FDiv fd_per, fd_gw, fd_sy, fd_sx, fd_cdiv, fd_cq;
 };
+
+inline void gemm_prepare(GemmArgs& g) {
+  g.fd_per = fdiv_make((uint32_t)(g.gh * g.gw));
+  g.fd_gw = fdiv_make((uint32_t)g.gw);
+  g.fd_sy = fdiv_make((uint32_t)g.sy);
+  g.fd_sx = fdiv_make((uint32_t)g.sx);
+  g.fd_cdiv = fdiv_make((uint32_t)g.cdiv);
+  g.fd_cq = fdiv_make((uint32_t)g.cq);
+}
 
 // BRES ("B resident", weight-stationary): every tile of the launch shares one B
 // (n_tiles == 1, splits == 1) whose K-blocks fit in kBResBytes of shared memory; it
@@ -83,16 +116,31 @@ constexpr uint32_t kBResBytes = 96 * 1024;
 
 constexpr uint32_t kWinBytes = 20 * 1024;  // window stage: up to 160 rows x 128 B
 
-template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0>
+// AU8 raw staging: per tile, 4 channel planes x up to 9 (img, gy) grid rows x 4 frame lines
+// of 84 bytes (one 336-byte span per grid row), copied by bulk TMA from the u8 frames
+constexpr int kRawRowBytes = 336;
+constexpr int kRawRows = 9;
+constexpr uint32_t kRawCiBytes = kRawRows * kRawRowBytes;  // 3024
+constexpr uint32_t kRawBytes = 12288;                       // >= 4 * 3024, 1 KB multiple
+constexpr int kRawStages = 4;
+constexpr int kConvWarps = 8;  // AU8 converter warps (after the epilogue warps)
+
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
 struct GemmCfg {
+  // two epilogue warpgroups take alternate tiles (4 TMEM accumulators) when 4 * BN fits
+  static constexpr int EPI = (4 * BN <= 512) ? 2 : 1;
+  static constexpr int ACC = 2 * EPI;
+  static constexpr int CONV_WARP0 = 4 + 4 * EPI;  // AU8 converter warps follow the epilogue
+  static constexpr int THREADS = 128 + 128 * EPI + (AU8 ? 32 * kConvWarps : 0);
   static constexpr uint32_t A_BYTES = AW ? kWinBytes : 128 * 64 * 2;
   static constexpr uint32_t B_BYTES = BN * 64 * 2;
   static constexpr uint32_t STAGE = BRES ? A_BYTES : A_BYTES + B_BYTES;
-  static constexpr uint32_t B_RES = BRES ? kBResBytes : 0;
-  static constexpr int STAGES = (200 * 1024 - B_RES) / STAGE > 8 ? 8 : (200 * 1024 - B_RES) / STAGE;
-  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)B_RES + (size_t)STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ +
-                                 4 * BN * sizeof(float) /*column sums*/;
+  static constexpr uint32_t B_RES = AU8 ? 16 * 1024 : BRES ? kBResBytes : 0;
+  static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
+  static constexpr int STAGES = (200 * 1024 - B_RES - RAW) / STAGE > 8 ? 8 : (200 * 1024 - B_RES - RAW) / STAGE;
+  static constexpr uint32_t TMEM_COLS = (ACC * BN <= 32) ? 32 : (ACC * BN <= 64) ? 64 : (ACC * BN <= 128) ? 128 : (ACC * BN <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)B_RES + RAW + (size_t)STAGES * STAGE + 1024 /*align*/ + 512 /*barriers*/ +
+                                 4 * EPI * BN * sizeof(float) /*column sums*/ + 128 /*raw barriers*/;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(BM == B_KMAJOR || BSWZ == 128 || (BSWZ == 64 && BN == 32), "B swizzle");
 };
@@ -103,7 +151,7 @@ BP_DEVICE unsigned long long gtimer() {
   return t;
 }
 BP_DEVICE void trace_ev(const GemmArgs& g, int i, int ev) {
-  if (g.trace && i < g.trace_tiles) g.trace[((size_t)blockIdx.x * g.trace_tiles + i) * 8 + ev] = gtimer();
+  if (g.trace && i < g.trace_tiles) g.trace[((size_t)blockIdx.x * g.trace_tiles + i) * 16 + ev] = gtimer();
 }
 
 BP_DEVICE void tile_coords(const GemmArgs& g, int tile, int& mt, int& nt, int& sp) {
@@ -197,13 +245,20 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
     }
     return;
   }
-  if (g.alpha != 1.f) {
+  if (g.bias) {  // alpha * acc + bias; the 32 bias values as 8 broadcast 16-byte loads
+    const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0);
+    const float al = g.alpha;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(b4 + q);
+      v[4 * q] = fmaf(v[4 * q], al, b.x);
+      v[4 * q + 1] = fmaf(v[4 * q + 1], al, b.y);
+      v[4 * q + 2] = fmaf(v[4 * q + 2], al, b.z);
+      v[4 * q + 3] = fmaf(v[4 * q + 3], al, b.w);
+    }
+  } else if (g.alpha != 1.f) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= g.alpha;
-  }
-  if (g.bias) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += __ldg(g.bias + n0 + i);
   }
   if (g.relu) {
 #pragma unroll
@@ -216,8 +271,9 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
       if (!((w >> i) & 1u)) v[i] = 0.f;
   }
   if (row_ok) {
-    const int qd = n0 / g.cdiv;
-    const long long cbase = (long long)(qd / g.cq) * g.cs1 + (long long)(qd % g.cq) * g.cs2 + (n0 % g.cdiv);
+    const uint32_t qd = fdivu((uint32_t)n0, g.fd_cdiv), q1 = fdivu(qd, g.fd_cq);
+    const long long cbase = (long long)q1 * g.cs1 + (long long)(qd - q1 * (uint32_t)g.cq) * g.cs2 +
+                            (long long)((uint32_t)n0 - qd * (uint32_t)g.cdiv);
     const long long off = rbase + cbase + (long long)sp * g.split_stride;
     if (g.bits_out) {
       uint32_t bits = 0;
@@ -248,33 +304,145 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
   }
 }
 
-template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// two u8 (bytes k, k+1 of w) -> packed bf16x2, exact: 0x4B0000bb as f32 is 2^23 + b
+BP_DEVICE uint32_t u8pair_bf16x2(uint32_t w, int k) {
+  const float lo = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k)) - 8388608.f;
+  const float hi = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k + 1)) - 8388608.f;
+  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632u);
+}
+
+// u8 plane of (img, ci) (AU8 frame source)
+BP_DEVICE const uint8_t* u8_plane(const GemmArgs& g, long long img, int ci) {
+  long long p = img * 4 + ci;
+  if (g.u8_index) {
+    const int q = __ldg(g.u8_index + p);
+    p = q < 0 ? 0 : q >= g.u8_planes ? g.u8_planes - 1 : q;
+  }
+  return g.u8 + p * 7056;
+}
+
+// AU8 producer (one warp): bulk-copy the frame lines behind grid rows [r0, r0 + nrows) into
+// a raw stage laid out [ci][grid row - G0][336 B]; lanes 0..7 each copy one (image, ci) span.
+BP_DEVICE void u8_stage_issue(const GemmArgs& g, long long r0, int nrows, uint8_t* raw, uint64_t* bar, int lane) {
+  const long long gmax = g.u8_rows / 21 - 1;  // last global grid row (img*21 + gy)
+  const long long G0 = r0 / 21;
+  long long G1 = (r0 + nrows - 1) / 21;
+  G1 = G1 > gmax ? gmax : G1;
+  // image segments: [G0, Gm] in image G0/21, [Gm+1, G1] in the next one
+  const long long img0 = G0 / 21;
+  const long long Gm = G1 < img0 * 21 + 20 ? G1 : img0 * 21 + 20;
+  const uint32_t bytes0 = (uint32_t)(Gm - G0 + 1) * kRawRowBytes;
+  const uint32_t bytes1 = G1 > Gm ? (uint32_t)(G1 - Gm) * kRawRowBytes : 0u;
+  if (lane == 0) sm100::mbar_arrive_expect_tx(bar, 4 * (bytes0 + bytes1));
+  __syncwarp();
+  if (lane < 8) {
+    const int ci = lane & 3, seg = lane >> 2;
+    const uint32_t bytes = seg ? bytes1 : bytes0;
+    if (bytes) {
+      const long long img = img0 + seg;
+      const int gy = seg ? 0 : (int)(G0 - img0 * 21);
+      const uint8_t* src = u8_plane(g, img, ci) + gy * kRawRowBytes;
+      uint8_t* dst = raw + ci * kRawCiBytes + (seg ? (uint32_t)(Gm - G0 + 1) * kRawRowBytes : 0u);
+      bulk_g2s(dst, src, bytes, bar);
+    }
+  }
+  __syncwarp();
+}
+
+// AU8 converters (kConvWarps warps, thread c): raw stage -> bf16 grid rows [r0, r0 + nrows)
+// in the 128B-swizzled K-major layout (row rr at rr * 128, 16-byte chunk j at j ^ (rr & 7)).
+// Explicit shared-space loads / stores (the stage pointers are generic).
+BP_DEVICE uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+// an opaque copy of a value, produced after the preceding (volatile) mbarrier wait, so that
+// non-volatile loads addressed through it cannot be hoisted above the wait
+BP_DEVICE uint32_t after_wait(uint32_t v) {
+  uint32_t o;
+  asm volatile("mov.b32 %0, %1;\n" : "=r"(o) : "r"(v) : "memory");
+  return o;
+}
+BP_DEVICE void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+BP_DEVICE void u8_stage_convert(const GemmArgs& g, long long r0, int nrows, const uint8_t* raw, uint8_t* a, int c,
+                                 int own_rows) {
+  constexpr int RSTEP = kConvWarps * 4;               // rows per pass (8 chunks per row)
+  constexpr int NIT = (160 + RSTEP - 1) / RSTEP;       // window rows <= 160
+  const int x0 = (int)(r0 % 21);                         // grid column of row r0
+  const int valid = (int)min((long long)nrows, g.u8_rows - r0);  // rows past the tensor -> 0
+  const uint32_t sraw = after_wait(sm100::smem_addr(raw)), sa = sm100::smem_addr(a);
+  const int j = c & 7;  // fixed chunk per thread
+  const uint32_t cbase = sraw + (j >> 1) * kRawCiBytes + (j & 1) * 2 * 84;
+  const int rr0 = c >> 3;
+  // all loads of this thread's rows first (independent), then convert + store
+  uint32_t w0[NIT], w1[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int rr = rr0 + it * RSTEP;
+    w0[it] = w1[it] = 0u;
+    if (rr < valid) {
+      const int q = x0 + rr;          // 32-bit: grid row offset G - G0 = q / 21, gx = q % 21
+      const int gs = q / 21;
+      const uint32_t src = cbase + gs * kRawRowBytes + 4 * (q - gs * 21);
+      w0[it] = lds_u32(src);
+      w1[it] = lds_u32(src + 84);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int rr = rr0 + it * RSTEP;
+    if (rr < nrows) {
+      const uint4 v = make_uint4(u8pair_bf16x2(w0[it], 0), u8pair_bf16x2(w0[it], 2), u8pair_bf16x2(w1[it], 0),
+                                 u8pair_bf16x2(w1[it], 2));
+      sts_v4(sa + rr * 128 + ((j ^ (rr & 7)) << 4), v.x, v.y, v.z, v.w);
+      // the tile's own rows (not the window halo) also to HBM: 128 B per row, coalesced
+      if (g.u8_x0_out && rr < own_rows && rr < valid)
+        __stcs(reinterpret_cast<uint4*>(g.u8_x0_out + (r0 + rr) * 64) + j, v);
+    }
+  }
+}
+
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
+__global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB) {
-  using C = GemmCfg<BN, AM, BM, BSWZ, BRES, AW>;
+  using C = GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>;
   static_assert(AW == 0 || (BRES && AM == A_KMAJOR), "window mode: K-major A with resident B");
+  static_assert(AU8 == 0 || AW > 0, "u8 A operand: window mode (conv1 forward)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* bres = smem;                // resident B (BRES): K-block kb at kb * B_BYTES
-  uint8_t* ring = smem + C::B_RES;     // pipeline stages
+  uint8_t* rawr = smem + C::B_RES;     // AU8 raw u8 stages
+  uint8_t* ring = rawr + C::RAW;       // pipeline stages
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
+  uint64_t* tempty = tfull + C::ACC;
+  uint64_t* bfull = tempty + C::ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
-  float* csum_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bfull) + 64);  // [4][BN]
+  float* csum_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bfull) + 64);  // [4 * EPI][BN]
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(csum_smem + 4 * C::EPI * BN);        // AU8
+  uint64_t* raw_empty = raw_full + kRawStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
     for (int s = 0; s < C::STAGES; ++s) {
-      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&full[s], AU8 ? kConvWarps : 1);  // AU8: one arrival per converter warp
       sm100::mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    if constexpr (AU8 > 0) {
+      for (int s = 0; s < kRawStages; ++s) {
+        sm100::mbar_init(&raw_full[s], 1);
+        sm100::mbar_init(&raw_empty[s], kConvWarps);
+      }
+    }
+    for (int i = 0; i < C::ACC; ++i) {
       sm100::mbar_init(&tfull[i], 1);
       sm100::mbar_init(&tempty[i], 4);
     }
@@ -309,7 +477,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int kb0 = sp * g.kb_per_split;
       const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
       if (lane == 0) trace_ev(g, ti, 0);
-      if constexpr (AW > 0) {  // one window per channel block feeds all taps
+      if constexpr (AU8 > 0) {  // raw frame lines of the window -> raw stage (converters build A)
+        sm100::mbar_wait(&raw_empty[stage], phase ^ 1);
+        u8_stage_issue(g, (long long)mt * 128 + g.a_min_off, g.a_win_rows, rawr + stage * kRawBytes,
+                       &raw_full[stage], lane);
+        if (++stage == kRawStages) { stage = 0; phase ^= 1; }
+      } else if constexpr (AW > 0) {  // one window per channel block feeds all taps
         for (int cb = 0; cb < g.a_cb; ++cb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           if (sm100::elect_one()) {
@@ -397,37 +570,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (sm100::elect_one()) sm100::umma_commit(&tfull[acc]);
       __syncwarp();
       if (lane == 0) trace_ev(g, ti, 3);
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (++acc == C::ACC) { acc = 0; aphase ^= 1; }
     }
-  } else if (warp >= 4) {
-    const int ew = warp - 4;
+  } else if (AU8 > 0 && warp >= C::CONV_WARP0) {
+    // converters: raw stage -> swizzled bf16 window in the A ring (one tile per stage)
+    const int c = threadIdx.x - 32 * C::CONV_WARP0;
+    int rs = 0, stage = 0;
+    uint32_t rph = 0, phase = 0;
+    int ti = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+      int mt, nt, sp;
+      tile_coords(g, tile, mt, nt, sp);
+      sm100::mbar_wait(&raw_full[rs], rph);
+      sm100::mbar_wait(&empty[stage], phase ^ 1);
+      if (c == 0) trace_ev(g, ti, 6);
+      u8_stage_convert(g, (long long)mt * 128 + g.a_min_off, g.a_win_rows, rawr + rs * kRawBytes,
+                       ring + stage * C::STAGE, c, 128 - g.a_min_off);
+      if (c == 0) trace_ev(g, ti, 8);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> UMMA reads
+      if (c == 0) trace_ev(g, ti, 9);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        sm100::mbar_arrive(&full[stage]);
+        sm100::mbar_arrive(&raw_empty[rs]);
+      }
+      if (c == 0) trace_ev(g, ti, 7);
+      if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+      if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp >= 4 && warp < 4 + 4 * C::EPI) {
+    // epilogue warpgroup grp takes the CTA's tiles k = grp, grp + EPI, ... (accumulator k % ACC);
+    // warp ew of a group reads TMEM lanes [32 ew, 32 ew + 32)
+    const int grp = (warp - 4) >> 2, ew = (warp - 4) & 3;
     constexpr int NCH = BN / 32;
-    int acc = 0;
-    uint32_t aphase = 0;
     // bias-gradient column sums: accumulated per CTA (per epilogue warp, in shared memory)
     // when every tile covers the same columns; otherwise written per tile
     const bool cta_colsum = g.colsum && g.n_tiles == 1 && g.splits == 1;
-    float* csum = csum_smem + ew * BN;
+    float* csum = csum_smem + (grp * 4 + ew) * BN;
     if (cta_colsum) {
       for (int c = 0; c < NCH; ++c) csum[c * 32 + lane] = 0.f;
     }
-    int ti = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+    for (int ti = grp, tile = blockIdx.x + grp * gridDim.x; tile < ntiles;
+         ti += C::EPI, tile += C::EPI * gridDim.x) {
+      const int acc = ti % C::ACC;
+      const uint32_t aphase = (uint32_t)(ti / C::ACC) & 1u;
       int mt, nt, sp;
       tile_coords(g, tile, mt, nt, sp);
       const int m = mt * 128 + ew * 32 + lane;
       // row map
       bool row_ok = m < g.M;
       long long rbase = 0;
-      {
-        const int per = g.gh * g.gw;
-        const int img = m / per;
-        const int rem = m - img * per;
-        const int y = rem / g.gw;
-        const int x = rem - y * g.gw;
-        row_ok = row_ok && (y < g.vh) && (x < g.vw);
-        rbase = (long long)img * g.r_img + (long long)(y / g.sy) * g.r_y + (long long)(x / g.sx) * g.r_x +
-                (long long)((y % g.sy) * g.sx + (x % g.sx)) * g.r_sub;
+      {  // precomputed-multiplier divisions (m < 2^31)
+        const uint32_t mu = (uint32_t)m;
+        const uint32_t img = fdivu(mu, g.fd_per);
+        const uint32_t rem = mu - img * (uint32_t)(g.gh * g.gw);
+        const uint32_t y = fdivu(rem, g.fd_gw);
+        const uint32_t x = rem - y * (uint32_t)g.gw;
+        const uint32_t ys = fdivu(y, g.fd_sy), xs = fdivu(x, g.fd_sx);
+        row_ok = row_ok && ((int)y < g.vh) && ((int)x < g.vw);
+        rbase = (long long)img * g.r_img + (long long)ys * g.r_y + (long long)xs * g.r_x +
+                (long long)((y - ys * (uint32_t)g.sy) * (uint32_t)g.sx + (x - xs * (uint32_t)g.sx)) * g.r_sub;
       }
       // prefetch the tile's relu-mask words (one u32 per 32 columns) before waiting for the
       // accumulator, so their latency overlaps the MMAs (masked GEMMs have BN <= 128)
@@ -459,12 +661,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (ew == 0 && lane == 0) trace_ev(g, ti, 5);
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
-    if (cta_colsum) {
-      __syncwarp();
-      for (int c = 0; c < NCH; ++c)
-        g.colsum[(size_t)(blockIdx.x * 4 + ew) * g.N + c * 32 + lane] = csum[c * 32 + lane];
+    if (cta_colsum) {  // fixed-order combine of the groups' sums, one row per lane quadrant
+      if constexpr (C::EPI > 1) asm volatile("bar.sync 2, %0;\n" ::"n"(128 * C::EPI) : "memory");
+      if (grp == 0) {
+        for (int c = 0; c < NCH; ++c) {
+          float v = csum[c * 32 + lane];
+          for (int q = 1; q < C::EPI; ++q) v += csum_smem[(q * 4 + ew) * BN + c * 32 + lane];
+          g.colsum[(size_t)(blockIdx.x * 4 + ew) * g.N + c * 32 + lane] = v;
+        }
+      }
     }
   }
   __syncthreads();
