@@ -203,6 +203,10 @@ int bp_gemm_trace_next(void* buf, int tiles);
  * (no bf16 space-to-depth grid in HBM); 0 uses the bf16 X0 grid.  Results are identical.
  * on < 0 only queries.  Returns the previous setting.  (Test / A-B knob, process-global.) */
 int bp_atari_set_conv1_u8(int on);
+/* Conv weight-gradient path: 1 (default) = window kernel (one X window + dY box per K-block
+ * feeds every m-tile of the CTA), 0 = per-tap operand boxes.  Identical sums in the same
+ * order per split; the split plan differs.  on < 0 queries.  Returns the previous setting. */
+int bp_atari_set_wgrad_window(int on);
 /* Forward with frame-stack dedup: the frames are not shipped as [n][4][84][84]
  * but as a plane store planes u8 [num_planes][84][84] (one plane per env step) and
  * plane_index int32 [n][4]: channel c of frame i is planes[plane_index[i*4 + c]]

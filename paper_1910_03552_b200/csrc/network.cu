@@ -108,9 +108,41 @@ static GemmArgs base_args() {
   return g;
 }
 
+// conv weight gradients through the window kernel (umma_wgrad_win_kernel); 0 = per-tap
+// atom boxes through umma_gemm_kernel (BP_WGRAD_WINDOW=0 / bp_atari_set_wgrad_window)
+static int g_wgrad_win = -1;
+static bool wgrad_window() {
+  if (g_wgrad_win < 0) {
+    const char* e = std::getenv("BP_WGRAD_WINDOW");
+    g_wgrad_win = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_wgrad_win != 0;
+}
+
 static void* g_trace_next = nullptr;
 static int g_trace_tiles = 0;
 
+template <int BN, int BSWZ, int NMT>
+static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUtensorMap& ty, cudaStream_t s) {
+  using Cfg = WgCfg<BN, BSWZ, NMT>;
+  auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT>;
+  WgArgs g = g0;
+  if (g.win_rows > 160 || g.a_cb > Cfg::MAX_CB || g.splits < 1) {
+    set_error("wgrad window: %d rows / %d channel blocks unsupported", g.win_rows, g.a_cb);
+    return BP_ERR_ARG;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) {
+      set_error("wgrad smem attr: %s", cudaGetErrorString(e));
+      return BP_ERR_LAUNCH;
+    }
+    attr = true;
+  }
+  kern<<<g.splits, 256, Cfg::SMEM, s>>>(g, tx, ty);
+  return check_launch("umma_wgrad_win_kernel");
+}
 template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
 static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
   GemmArgs g = g0;
@@ -368,8 +400,9 @@ struct NetPlan {
   size_t total_floats;
 };
 
-static void make_plan(int n, int sms, NetPlan* P) {
+static void make_plan(int n, int sms, NetPlan* P, bool win) {
   const long long rows[4] = {(long long)n * 441, (long long)n * 100, (long long)n * 81, n};
+  // conv3's 9 taps x 64 channels pad to 5 m-tiles (the 10th atom is the zero atom)
   const int M[4] = {256, 512, 576, kCoreW};
   const int Ns[4] = {32, 64, 64, 64};
   size_t off = 0;
@@ -378,7 +411,7 @@ static void make_plan(int n, int sms, NetPlan* P) {
     w.m_tiles = (M[i] + 127) / 128;
     w.n_tiles = 1;
     w.num_kb = (int)((rows[i] + 63) / 64);
-    int sp = (sms + w.m_tiles - 1) / w.m_tiles;
+    int sp = (i < 3 && win) ? sms : (sms + w.m_tiles - 1) / w.m_tiles;
     if (sp > w.num_kb) sp = w.num_kb;
     if (sp < 1) sp = 1;
     w.kb_per = (w.num_kb + sp - 1) / sp;
@@ -526,6 +559,12 @@ extern "C" int bp_gemm_trace_next(void* buf, int tiles) {
   return BP_OK;
 }
 
+extern "C" int bp_atari_set_wgrad_window(int on) {
+  const int prev = wgrad_window() ? 1 : 0;
+  if (on >= 0) g_wgrad_win = on ? 1 : 0;
+  return prev;
+}
+
 extern "C" int bp_atari_set_conv1_u8(int on) {
   const int prev = conv1_u8() ? 1 : 0;
   if (on >= 0) g_conv1_u8 = on ? 1 : 0;
@@ -551,9 +590,10 @@ extern "C" int bp_atari_param_offsets(int num_actions, int use_lstm, int64_t* of
 extern "C" size_t bp_atari_workspace_bytes(int num_actions, int max_frames) {
   (void)num_actions;
   if (init_driver()) return 0;
-  NetPlan P;
-  make_plan(max_frames, g_num_sms, &P);
-  return P.total_floats * sizeof(float);
+  NetPlan P, Q;  // sized for either weight-gradient mode (bp_atari_set_wgrad_window)
+  make_plan(max_frames, g_num_sms, &P, true);
+  make_plan(max_frames, g_num_sms, &Q, false);
+  return (P.total_floats > Q.total_floats ? P.total_floats : Q.total_floats) * sizeof(float);
 }
 
 static int check_net(const BpAtariNet* net, int n) {
@@ -898,15 +938,52 @@ static int torso_backward(const BpAtariNet* net, int n, const void* head_in, flo
     if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
     return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
   };
+  // conv weight gradients, window kernel: X window + dY box per K-block feed every m-tile
+  auto wgrad_win = [&](int i, const void* X, long long xrows, int xcols, int nshifts, const int* offs,
+                       const void* dY, int ncols) -> int {
+    const WgPlan& w = P.wg[i];
+    WgArgs g;
+    memset(&g, 0, sizeof(g));
+    g.num_kb = w.num_kb;
+    g.kb_per_split = w.kb_per;
+    g.splits = w.splits;
+    g.a_cb = xcols / 64;
+    g.nshifts = nshifts;
+    g.atoms_per_shift = xcols / 64;
+    int mx = 0;
+    for (int k = 0; k < nshifts; ++k) {
+      g.row_off[k] = offs[k];
+      mx = offs[k] > mx ? offs[k] : mx;
+    }
+    g.min_off = 0;
+    g.win_rows = (64 + mx + 7) & ~7;
+    g.Mpad = (int)w.Mpad;
+    g.N = w.Npad;
+    g.out = ws + w.off;
+    int r;
+    if ((r = make_tmap(&ta, X, xrows, xcols, 64, g.win_rows, 128))) return r;
+    if (ncols == 32) {
+      if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
+      return launch_wgrad_win<32, 64, 2>(g, ta, tb, s);
+    }
+    if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
+    return i == 1 ? launch_wgrad_win<64, 128, 4>(g, ta, tb, s) : launch_wgrad_win<64, 128, 5>(g, ta, tb, s);
+  };
   {
     const int o1[4] = {0, 1, 21, 22};
-    if ((rc = wgrad(0, net->x0, (long long)n * 441, 64, 1, 4, o1, net->d_pre1, 32))) return rc;
     const int o2[4] = {0, 1, 10, 11};
-    if ((rc = wgrad(1, net->x1, (long long)n * 100, 128, 2, 4, o2, net->d_pre2, 64))) return rc;
     int o3[9];
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) o3[dy * 3 + dx] = dy * 9 + dx;
-    if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
+    if (wgrad_window()) {
+      if ((rc = wgrad_win(0, net->x0, (long long)n * 441, 64, 4, o1, net->d_pre1, 32))) return rc;
+      if ((rc = wgrad_win(1, net->x1, (long long)n * 100, 128, 4, o2, net->d_pre2, 64))) return rc;
+      if ((rc = wgrad_win(2, net->x2, (long long)n * 81, 64, 9, o3, net->d_pre3, 64))) return rc;
+    } else {
+      if ((rc = wgrad(0, net->x0, (long long)n * 441, 64, 1, 4, o1, net->d_pre1, 32))) return rc;
+      if ((rc = wgrad(1, net->x1, (long long)n * 100, 128, 2, 4, o2, net->d_pre2, 64))) return rc;
+      if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
+    }
     const int o0[1] = {0};
     if ((rc = wgrad(3, head_in, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
   }
@@ -963,7 +1040,7 @@ static int torso_backward(const BpAtariNet* net, int n, const void* head_in, flo
 }
 
 static int plan_for(const BpAtariNet* net, int n, NetPlan* P) {
-  make_plan(n, g_num_sms, P);
+  make_plan(n, g_num_sms, P, wgrad_window());
   if (P->total_floats * sizeof(float) > net->ws_bytes) {
     set_error("atari backward: workspace %zu < %zu bytes", net->ws_bytes, P->total_floats * sizeof(float));
     return BP_ERR_ARG;

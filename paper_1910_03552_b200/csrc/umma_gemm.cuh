@@ -680,4 +680,190 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
   }
 }
 
+// ============================================================================
+// Weight-gradient "window" GEMM (conv weight gradients):
+//   D[m][n] = sum_rows X[row + off(m)][c(m)] * dY[row][n],  m = (tap, channel)
+// reduced over grid rows in K-blocks of 64.  Per K-block the producer loads ONE window of
+// X rows [kb*64 + min_off, kb*64 + 64 + max_off) per 64-channel block (plus the dY box), and
+// every M atom (tap, channel block) of every m-tile is a view into it: an M=128 MMA covers
+// atoms (2mt, 2mt+1) with the A descriptor at atom 2mt and LBO = address(2mt+1) - address(2mt)
+// (MN-major, 128B swizzle on absolute smem addresses, like the forward window mode).  One
+// CTA owns all NMT m-tiles of its K range (NMT accumulators in TMEM), so X and dY cross
+// L2 -> SM once per K-block instead of once per (m-tile, tap).
+// Output: f32 partials out[split][Mpad][N] (split = the CTA's K range), reduced by finalize.
+// ============================================================================
+struct WgArgs {
+  int num_kb, kb_per_split, splits;
+  int a_cb;                       // 64-channel blocks of X (window count per stage)
+  int nshifts, atoms_per_shift;   // atom a -> tap a / atoms_per_shift, block a % atoms_per_shift
+  int row_off[kMaxShifts];        // per-tap row offset (>= 0)
+  int min_off, win_rows;          // window rows (multiple of 8)
+  int Mpad, N;
+  float* out;
+  unsigned long long* trace;
+  int trace_tiles;
+};
+
+template <int BN, int BSWZ, int NMT>
+struct WgCfg {
+  static constexpr uint32_t WIN_BYTES = 160 * 128;  // <= 160 window rows per channel block
+  static constexpr uint32_t B_BYTES = BN * 64 * 2;
+  static constexpr int MAX_CB = 2;
+  static constexpr uint32_t STAGE = MAX_CB * WIN_BYTES + B_BYTES;  // 1 KB multiple
+  static constexpr uint32_t ZERO = 8192;                           // the all-zero atom
+  static constexpr int STAGES = (200 * 1024 - ZERO) / STAGE > 6 ? 6 : (200 * 1024 - ZERO) / STAGE;
+  static constexpr uint32_t TMEM_COLS = (NMT * BN <= 32) ? 32 : (NMT * BN <= 64) ? 64 : (NMT * BN <= 128) ? 128
+                                        : (NMT * BN <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + 1024 + 256;
+  static_assert(NMT * BN <= 512, "TMEM");
+};
+
+template <int BN, int BSWZ, int NMT>
+__global__ void __launch_bounds__(256, 1)
+    umma_wgrad_win_kernel(const __grid_constant__ WgArgs g, const __grid_constant__ CUtensorMap tmX,
+                          const __grid_constant__ CUtensorMap tmY) {
+  using C = WgCfg<BN, BSWZ, NMT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;                           // stages: [windows | dY box]
+  uint8_t* zero = ring + C::STAGES * C::STAGE;    // all-zero atom (above the ring: LBO > 0)
+  uint64_t* full = reinterpret_cast<uint64_t*>(zero + C::ZERO);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (int)(C::ZERO / 16); i += blockDim.x)
+    reinterpret_cast<uint4*>(zero)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmX);
+    sm100::tma_prefetch_desc(&tmY);
+    for (int s = 0; s < C::STAGES; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(tfull, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t stage_tx = g.a_cb * g.win_rows * 128 + C::B_BYTES;
+
+  if (warp == 0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
+      const int kb0 = sp * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        if (sm100::elect_one()) {
+          uint8_t* st = ring + stage * C::STAGE;
+          sm100::mbar_arrive_expect_tx(&full[stage], stage_tx);
+          for (int cb = 0; cb < g.a_cb; ++cb)
+            sm100::tma_load_2d(st + cb * C::WIN_BYTES, &tmX, &full[stage], cb * 64, kb * 64 + g.min_off);
+          uint8_t* sb = st + C::MAX_CB * C::WIN_BYTES;
+          if constexpr (BSWZ == 64) {
+            sm100::tma_load_2d(sb, &tmY, &full[stage], 0, kb * 64);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, &tmY, &full[stage], j * 64, kb * 64);
+          }
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = sm100::idesc_bf16(128, BN, true, true);
+    const uint64_t b_hi = BSWZ == 64 ? sm100::smem_desc(0, 16, 512, sm100::SWZ_64B)
+                                     : sm100::smem_desc(0, 8192, 1024, sm100::SWZ_128B);
+    constexpr uint32_t b_kstep = BSWZ == 64 ? 1024 : 2048;
+    // per m-tile: A start offset (within a stage; bit 31 = the zero atom) and LBO
+    uint32_t a_off[NMT], a_lbo[NMT];
+    const uint32_t zero_addr = sm100::smem_addr(zero);
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) {
+      uint32_t ad[2];
+      bool z[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int atom = 2 * mt + j;
+        const int sft = atom / g.atoms_per_shift, cb = atom - sft * g.atoms_per_shift;
+        z[j] = sft >= g.nshifts;
+        ad[j] = z[j] ? 0u : cb * C::WIN_BYTES + (uint32_t)(g.row_off[sft] - g.min_off) * 128u;
+      }
+      a_off[mt] = ad[0];
+      a_lbo[mt] = z[1] ? 0xffffffffu : ad[1] - ad[0];  // zero atom: resolved per stage below
+    }
+    // one K range (split) per CTA: grid == splits (single accumulator set)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
+      const int kb0 = sp * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&full[stage], phase);
+        sm100::tc_fence_after();
+        const uint32_t st = sm100::smem_addr(ring + stage * C::STAGE);
+        const uint32_t sb = st + C::MAX_CB * C::WIN_BYTES;
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int mt = 0; mt < NMT; ++mt) {
+            const uint32_t sa = st + a_off[mt];
+            const uint32_t lbo = a_lbo[mt] == 0xffffffffu ? zero_addr - sa : a_lbo[mt];
+            const uint64_t a_hi = sm100::smem_desc(0, lbo, 1024, sm100::SWZ_128B);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              sm100::umma_f16(tmem_base + mt * BN, a_hi | ((sa + k * 2048) >> 4),
+                              b_hi | ((sb + k * b_kstep) >> 4), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          sm100::umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (sm100::elect_one()) sm100::umma_commit(tfull);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int ti = 0;
+    for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x, ++ti) {
+      const int kb0 = sp * g.kb_per_split;
+      const bool has_k = kb0 < g.num_kb;
+      if (has_k) {
+        sm100::mbar_wait(tfull, ti & 1);
+        sm100::tc_fence_after();
+      }
+#pragma unroll 1
+      for (int mt = 0; mt < NMT; ++mt) {
+        const int m = mt * 128 + ew * 32 + lane;
+        float* orow = g.out + ((size_t)sp * g.Mpad + m) * g.N;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          if (has_k) {
+            sm100::tmem_ld_32x32b_x32(tmem_base + mt * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
+            sm100::tmem_ld_wait();
+          }
+          float4* o = reinterpret_cast<float4*>(orow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            o[q] = has_k ? make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      sm100::tc_fence_before();
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
 }  // namespace bp
