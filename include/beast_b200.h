@@ -169,7 +169,13 @@ typedef struct BpAtariNet {
   void* d_pre1; /* [N*441][32]  conv1 pre-activation grad    */
   void* ws;     /* f32 workspace, bp_atari_workspace_bytes()  */
   size_t ws_bytes;
+  int flags;    /* BP_NET_* */
 } BpAtariNet;
+
+/* flags: the forward does not materialise the bf16 X0 grid (conv1 reads the u8 frames on
+ * chip); the backward then needs the same frame source: bp_atari_backward_frames.
+ * (LSTM nets ignore it: bp_atari_lstm_backward reads X0.) */
+#define BP_NET_NO_X0 1
 
 /* f32 master parameter layout (flat, upstream AtariNet module order):
  * [0] conv1.weight, [1] conv1.bias, [2] conv2.weight, [3] conv2.bias, [4] conv3.weight,
@@ -221,6 +227,12 @@ int bp_atari_forward_planes(const BpAtariNet* net, int n, const uint8_t* planes,
  * same layout as params; every entry is overwritten). */
 int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
                       const float* reward, const int64_t* last_action, float* grads, void* stream);
+/* Backward of the last forward given its frame source again (frames, or the plane store +
+ * plane index of bp_atari_forward_planes): the conv1 weight gradient converts the u8 frames
+ * on chip, so a BP_NET_NO_X0 net never writes or reads the bf16 X0 grid. */
+int bp_atari_backward_frames(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
+                             int num_planes, const float* d_logits, const float* d_baseline, float* grads,
+                             void* stream);
 
 /* ---------------------------------------------------------------------------
  * LSTM core (AtariNet(use_lstm=True): upstream nn.LSTM(H, H, 2), H = 513 + A,

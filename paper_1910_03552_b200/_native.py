@@ -46,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_gemm_trace_next": (I, [P, I]),
     "bp_atari_forward_planes": (I, [P, I, P, P, I, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
+    "bp_atari_backward_frames": (I, [P, I, P, P, I, P, P, P, P]),
     "bp_lstm_partial_floats": (SZ, [I]),
     "bp_lstm_trace": (I, [P]),
     "bp_lstm_set_mode": (I, [I]),
@@ -58,6 +59,9 @@ SIGNATURES: dict[str, tuple] = {
 }
 
 
+BP_NET_NO_X0 = 1
+
+
 class BpAtariNet(C.Structure):
     """Mirror of `BpAtariNet` in include/beast_b200.h (field order matters)."""
 
@@ -65,7 +69,7 @@ class BpAtariNet(C.Structure):
         (name, C.c_void_p) for name in (
             "wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
             "d_pre3", "d_pre2", "d_pre1", "ws")
-    ] + [("ws_bytes", C.c_size_t)]
+    ] + [("ws_bytes", C.c_size_t), ("flags", C.c_int)]
 
 
 class BpLstmCore(C.Structure):

@@ -117,8 +117,11 @@ class _Buffers:
         self.t["ws"] = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=d)
         names = ("wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
                  "d_pre3", "d_pre2", "d_pre1", "ws")
+        # conv1's forward converts the u8 frames on chip and writes the bf16 X0 grid as a side
+        # output for the weight gradient (flags=BP_NET_NO_X0 would convert again in the
+        # backward instead; measured slower)
         self.struct = N.BpAtariNet(num_actions, capacity, int(use_lstm),
-                                   *[self.t[k].data_ptr() for k in names], ws_bytes)
+                                   *[self.t[k].data_ptr() for k in names], ws_bytes, 0)
         self.ref = C.byref(self.struct)
         self.lstm = _LstmBuffers(num_actions, capacity, device) if use_lstm else None
 
@@ -329,6 +332,8 @@ class AtariNet(nn.Module):
             else:
                 N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), *tail), "bp_atari_forward")
         self._last_n = n
+        # frame source of this forward, for the backward (kept alive until the next forward)
+        self._frame_src = (frames, plane_index, num_planes if plane_index is not None else 0)
         return logits, baseline
 
     def _backward_kernels(self, d_logits, d_baseline, reward, last_action, grads, lstm: dict | None = None):
@@ -343,8 +348,13 @@ class AtariNet(nn.Module):
                 N.ptr(lstm["done"]), N.ptr(self.flat_params), N.ptr(lstm["c0"]), N.ptr(grads), stream),
                 "bp_atari_lstm_backward")
             return
-        N.check(N.lib().bp_atari_backward(b.ref, n, N.ptr(d_logits), N.ptr(d_baseline), N.ptr(reward),
-                                          N.ptr(last_action), N.ptr(grads), stream), "bp_atari_backward")
+        src = getattr(self, "_frame_src", None)
+        if src is None:
+            raise DimensionError("backward without a preceding forward")
+        frames, plane_index, num_planes = src
+        N.check(N.lib().bp_atari_backward_frames(b.ref, n, N.ptr(frames), N.ptr(plane_index), num_planes,
+                                                 N.ptr(d_logits), N.ptr(d_baseline), N.ptr(grads), stream),
+                "bp_atari_backward_frames")
 
     def sample(self, logits: torch.Tensor, greedy: bool) -> torch.Tensor:
         """Gumbel-max categorical sample (training) or argmax (eval), one kernel."""

@@ -122,10 +122,10 @@ static bool wgrad_window() {
 static void* g_trace_next = nullptr;
 static int g_trace_tiles = 0;
 
-template <int BN, int BSWZ, int NMT>
+template <int BN, int BSWZ, int NMT, int AU8 = 0>
 static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUtensorMap& ty, cudaStream_t s) {
-  using Cfg = WgCfg<BN, BSWZ, NMT>;
-  auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT>;
+  using Cfg = WgCfg<BN, BSWZ, NMT, AU8>;
+  auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT, AU8>;
   WgArgs g = g0;
   if (g.win_rows > 160 || g.a_cb > Cfg::MAX_CB || g.splits < 1) {
     set_error("wgrad window: %d rows / %d channel blocks unsupported", g.win_rows, g.a_cb);
@@ -140,13 +140,14 @@ static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUten
     }
     attr = true;
   }
-  kern<<<g.splits, 256, Cfg::SMEM, s>>>(g, tx, ty);
+  kern<<<g.splits, Cfg::THREADS, Cfg::SMEM, s>>>(g, tx, ty);
   return check_launch("umma_wgrad_win_kernel");
 }
 template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
 static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
   GemmArgs g = g0;
   gemm_prepare(g);
+
   if (g_trace_next) {  // debug: per-tile role timeline of this launch (bp_gemm_trace_next)
     g.trace = reinterpret_cast<unsigned long long*>(g_trace_next);
     g.trace_tiles = g_trace_tiles;
@@ -375,6 +376,19 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
     const float* p = j.partial + m * j.Npad + n;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     int r = 0;
+    // 16 loads in flight per thread; the sums keep the fixed r mod 4 order
+    for (; r + 16 <= j.splits; r += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __ldcs(p + (long long)(r + q) * pstride);
+#pragma unroll
+      for (int q = 0; q < 16; q += 4) {
+        s0 += v[q];
+        s1 += v[q + 1];
+        s2 += v[q + 2];
+        s3 += v[q + 3];
+      }
+    }
     for (; r + 4 <= j.splits; r += 4) {
       s0 += p[(long long)r * pstride];
       s1 += p[(long long)(r + 1) * pstride];
@@ -653,7 +667,7 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
       g.u8_index = plane_index;
       g.u8_planes = num_planes;
       g.u8_rows = R;
-      g.u8_x0_out = bf(net->x0);
+      g.u8_x0_out = (net->flags & BP_NET_NO_X0) ? nullptr : bf(net->x0);
     } else if ((rc = make_tmap(&ta, net->x0, R, 64, 64, g.a_win_rows, 128))) {
       return rc;
     }
@@ -839,7 +853,15 @@ static int heads_backward(const BpAtariNet* net, int n, const float* d_logits, c
 
 // d_fc -> conv torso data / weight gradients, heads weight gradient (A operand head_in),
 // deterministic finalize of every partial into grads
-static int torso_backward(const BpAtariNet* net, int n, const void* head_in, float* grads, const int64_t* off,
+// the u8 frame source of the forward (for the conv1 weight gradient without an X0 grid)
+struct FrameSrc {
+  const uint8_t* frames;
+  const int32_t* plane_index;
+  int num_planes;
+};
+
+static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, const void* head_in, float* grads,
+                          const int64_t* off,
                           const NetPlan& P, float* ws, cudaStream_t s) {
   const int A = net->num_actions;
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
@@ -975,12 +997,38 @@ static int torso_backward(const BpAtariNet* net, int n, const void* head_in, flo
     int o3[9];
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) o3[dy * 3 + dx] = dy * 9 + dx;
-    if (wgrad_window()) {
+    if (src && conv1_u8() && (net->flags & BP_NET_NO_X0)) {
+      // conv1: windows converted on chip from the u8 frames (no X0 grid)
+      const WgPlan& w = P.wg[0];
+      WgArgs g;
+      memset(&g, 0, sizeof(g));
+      g.num_kb = w.num_kb;
+      g.kb_per_split = w.kb_per;
+      g.splits = w.splits;
+      g.a_cb = 1;
+      g.nshifts = 4;
+      g.atoms_per_shift = 1;
+      for (int k = 0; k < 4; ++k) g.row_off[k] = o1[k];
+      g.min_off = 0;
+      g.win_rows = (64 + 22 + 7) & ~7;
+      g.Mpad = (int)w.Mpad;
+      g.N = w.Npad;
+      g.out = ws + w.off;
+      g.u8 = src->frames;
+      g.u8_index = src->plane_index;
+      g.u8_planes = src->num_planes;
+      g.u8_rows = (long long)n * 441;
+      if ((rc = make_tmap(&tb, net->d_pre1, (long long)n * 441, 32, 32, 64, 64))) return rc;
+      if ((rc = launch_wgrad_win<32, 64, 2, 1>(g, tb, tb, s))) return rc;
+    } else if (wgrad_window()) {
       if ((rc = wgrad_win(0, net->x0, (long long)n * 441, 64, 4, o1, net->d_pre1, 32))) return rc;
+    } else if ((rc = wgrad(0, net->x0, (long long)n * 441, 64, 1, 4, o1, net->d_pre1, 32))) {
+      return rc;
+    }
+    if (wgrad_window()) {
       if ((rc = wgrad_win(1, net->x1, (long long)n * 100, 128, 4, o2, net->d_pre2, 64))) return rc;
       if ((rc = wgrad_win(2, net->x2, (long long)n * 81, 64, 9, o3, net->d_pre3, 64))) return rc;
     } else {
-      if ((rc = wgrad(0, net->x0, (long long)n * 441, 64, 1, 4, o1, net->d_pre1, 32))) return rc;
       if ((rc = wgrad(1, net->x1, (long long)n * 100, 128, 2, 4, o2, net->d_pre2, 64))) return rc;
       if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
     }
@@ -1033,7 +1081,7 @@ static int torso_backward(const BpAtariNet* net, int n, const void* head_in, flo
     f.bp_grad = grads + off[P_BP];
     f.wv_grad = grads + off[P_WV];
     f.bv_grad = grads + off[P_BV];
-    finalize_kernel<<<dim3(148, k), 256, 0, s>>>(f);
+    finalize_kernel<<<dim3(4 * g_num_sms, k), 256, 0, s>>>(f);
     if ((rc = check_launch("finalize_kernel"))) return rc;
   }
   return BP_OK;
@@ -1048,12 +1096,13 @@ static int plan_for(const BpAtariNet* net, int n, NetPlan* P) {
   return BP_OK;
 }
 
-extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits,
-                                 const float* d_baseline, const float* reward,
-                                 const int64_t* last_action, float* grads, void* stream) {
-  (void)reward;
-  (void)last_action;  // (their contribution to the heads gradient comes from the augmented core)
+static int atari_backward(const BpAtariNet* net, int n, const FrameSrc* src, const float* d_logits,
+                          const float* d_baseline, float* grads, void* stream) {
   if (int e = check_net(net, n)) return e;
+  if (!src && (net->flags & BP_NET_NO_X0) && conv1_u8()) {
+    set_error("atari: this net keeps no X0 grid (BP_NET_NO_X0): use bp_atari_backward_frames");
+    return BP_ERR_ARG;
+  }
   if (net->use_lstm) {
     set_error("atari: LSTM net -> bp_atari_lstm_backward");
     return BP_ERR_ARG;
@@ -1066,7 +1115,23 @@ extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_lo
   if ((rc = plan_for(net, n, &P))) return rc;
   float* ws = reinterpret_cast<float*>(net->ws);
   if ((rc = heads_backward(net, n, d_logits, d_baseline, P, ws, nullptr, s))) return rc;
-  return torso_backward(net, n, net->core, grads, off, P, ws, s);
+  return torso_backward(net, n, src, net->core, grads, off, P, ws, s);
+}
+
+extern "C" int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits,
+                                 const float* d_baseline, const float* reward,
+                                 const int64_t* last_action, float* grads, void* stream) {
+  (void)reward;
+  (void)last_action;  // (their contribution to the heads gradient comes from the augmented core)
+  return atari_backward(net, n, nullptr, d_logits, d_baseline, grads, stream);
+}
+
+extern "C" int bp_atari_backward_frames(const BpAtariNet* net, int n, const uint8_t* frames,
+                                        const int32_t* plane_index, int num_planes, const float* d_logits,
+                                        const float* d_baseline, float* grads, void* stream) {
+  if (int e = check_planes(frames, plane_index, num_planes)) return e;
+  const FrameSrc src{frames, plane_index, num_planes};
+  return atari_backward(net, n, &src, d_logits, d_baseline, grads, stream);
 }
 
 // ============================================================ LSTM core
@@ -1335,7 +1400,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   lstm_dfc_kernel<<<P.cs_rows[3], 256, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
                                                reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);
   if ((rc = check_launch("lstm_dfc_kernel"))) return rc;
-  return torso_backward(net, n, bfp(core->out, 1), grads, off, P, ws, s);
+  return torso_backward(net, n, nullptr, bfp(core->out, 1), grads, off, P, ws, s);
 }
 
 // ============================================================ action sampling

@@ -9,7 +9,7 @@
 namespace bp {
 
 constexpr int kOptThreads = 256;
-constexpr int kSumsqBlocks = 2 * 148;
+constexpr int kSumsqBlocks = 8 * 148;
 
 __global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
                                                             double* __restrict__ out,
@@ -46,12 +46,20 @@ __global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restr
     is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {
+  if (is_last) {  // the last block reduces the partials: fixed strided split + fixed tree
     __threadfence();
     double s = 0;
-    for (int k = 0; k < (int)gridDim.x; ++k) s += ((volatile double*)partials)[k];
-    *out = s;
-    *counter = 0u;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += kOptThreads) s += ((volatile double*)partials)[k];
+    s = warp_sum(s);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0;
+      for (int k = 0; k < kOptThreads / 32; ++k) t += red[k];
+      *out = t;
+      *counter = 0u;
+    }
   }
 }
 
@@ -168,7 +176,7 @@ extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_av
     return BP_ERR_ARG;
   }
   int64_t want = (n / 4 + kOptThreads - 1) / kOptThreads;
-  int grid = (int)(want < 1 ? 1 : (want > 4 * 148 ? 4 * 148 : want));
+  int grid = (int)(want < 1 ? 1 : (want > 8 * 148 ? 8 * 148 : want));
   rmsprop_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(
       params, grads, square_avg, n, sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps,
       write_clipped_grads, norm_out, reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status);

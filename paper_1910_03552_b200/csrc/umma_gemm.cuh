@@ -96,7 +96,7 @@ struct GemmArgs {
   __nv_bfloat16* u8_x0_out;  // optional: the converted grid rows of every tile also go to HBM
                              // as X0 [rows][64] bf16 (the conv1 weight-gradient operand)
   // epilogue divisors (filled by the launcher from gh*gw, gw, sy, sx, cdiv, cq)
-  FDiv fd_per, fd_gw, fd_sy, fd_sx, fd_cdiv, fd_cq;
+  FDiv fd_per, fd_gw, fd_sy, fd_sx, fd_cdiv, fd_cq, fd_splits, fd_ntiles;
 };
 
 inline void gemm_prepare(GemmArgs& g) {
@@ -106,6 +106,8 @@ inline void gemm_prepare(GemmArgs& g) {
   g.fd_sx = fdiv_make((uint32_t)g.sx);
   g.fd_cdiv = fdiv_make((uint32_t)g.cdiv);
   g.fd_cq = fdiv_make((uint32_t)g.cq);
+  g.fd_splits = fdiv_make((uint32_t)g.splits);
+  g.fd_ntiles = fdiv_make((uint32_t)g.n_tiles);
 }
 
 // BRES ("B resident", weight-stationary): every tile of the launch shares one B
@@ -155,10 +157,10 @@ BP_DEVICE void trace_ev(const GemmArgs& g, int i, int ev) {
 }
 
 BP_DEVICE void tile_coords(const GemmArgs& g, int tile, int& mt, int& nt, int& sp) {
-  sp = tile % g.splits;
-  const int r = tile / g.splits;
-  nt = r % g.n_tiles;
-  mt = r / g.n_tiles;
+  const uint32_t r = fdivu((uint32_t)tile, g.fd_splits);
+  sp = tile - (int)r * g.splits;
+  mt = (int)fdivu(r, g.fd_ntiles);
+  nt = (int)r - mt * g.n_tiles;
 }
 
 template <int AM>
@@ -312,7 +314,8 @@ BP_DEVICE uint32_t u8pair_bf16x2(uint32_t w, int k) {
 }
 
 // u8 plane of (img, ci) (AU8 frame source)
-BP_DEVICE const uint8_t* u8_plane(const GemmArgs& g, long long img, int ci) {
+template <class Args>
+BP_DEVICE const uint8_t* u8_plane(const Args& g, long long img, int ci) {
   long long p = img * 4 + ci;
   if (g.u8_index) {
     const int q = __ldg(g.u8_index + p);
@@ -323,7 +326,8 @@ BP_DEVICE const uint8_t* u8_plane(const GemmArgs& g, long long img, int ci) {
 
 // AU8 producer (one warp): bulk-copy the frame lines behind grid rows [r0, r0 + nrows) into
 // a raw stage laid out [ci][grid row - G0][336 B]; lanes 0..7 each copy one (image, ci) span.
-BP_DEVICE void u8_stage_issue(const GemmArgs& g, long long r0, int nrows, uint8_t* raw, uint64_t* bar, int lane) {
+template <class Args>
+BP_DEVICE void u8_stage_issue(const Args& g, long long r0, int nrows, uint8_t* raw, uint64_t* bar, int lane) {
   const long long gmax = g.u8_rows / 21 - 1;  // last global grid row (img*21 + gy)
   const long long G0 = r0 / 21;
   long long G1 = (r0 + nrows - 1) / 21;
@@ -368,12 +372,16 @@ BP_DEVICE void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
-BP_DEVICE void u8_stage_convert(const GemmArgs& g, long long r0, int nrows, const uint8_t* raw, uint8_t* a, int c,
+template <class Args, int CW = kConvWarps>
+BP_DEVICE void u8_stage_convert(const Args& g, long long r0, int nrows, const uint8_t* raw, uint8_t* a, int c,
                                  int own_rows) {
-  constexpr int RSTEP = kConvWarps * 4;               // rows per pass (8 chunks per row)
+  constexpr int RSTEP = CW * 4;                        // rows per pass (8 chunks per row)
   constexpr int NIT = (160 + RSTEP - 1) / RSTEP;       // window rows <= 160
-  const int x0 = (int)(r0 % 21);                         // grid column of row r0
-  const int valid = (int)min((long long)nrows, g.u8_rows - r0);  // rows past the tensor -> 0
+  // 32-bit grid-row arithmetic (grid rows < 2^31)
+  const uint32_t r0u = (uint32_t)r0;
+  const int x0 = (int)(r0u - fdivu(r0u, FDiv{0x86186187u, 5u}) * 21u);  // r0 % 21 (r0 < 2^31)
+  const long long left = g.u8_rows - r0;
+  const int valid = left < nrows ? (int)left : nrows;    // rows past the tensor -> 0
   const uint32_t sraw = after_wait(sm100::smem_addr(raw)), sa = sm100::smem_addr(a);
   const int j = c & 7;  // fixed chunk per thread
   const uint32_t cbase = sraw + (j >> 1) * kRawCiBytes + (j & 1) * 2 * 84;
@@ -702,35 +710,46 @@ struct WgArgs {
   float* out;
   unsigned long long* trace;
   int trace_tiles;
+  // AU8 (conv1): the X windows are converted on chip from u8 frames (see GemmArgs)
+  const uint8_t* u8;
+  const int32_t* u8_index;
+  int u8_planes;
+  long long u8_rows;
+  __nv_bfloat16* u8_x0_out;  // (unused here)
 };
 
-template <int BN, int BSWZ, int NMT>
+template <int BN, int BSWZ, int NMT, int AU8 = 0>
 struct WgCfg {
   static constexpr uint32_t WIN_BYTES = 160 * 128;  // <= 160 window rows per channel block
   static constexpr uint32_t B_BYTES = BN * 64 * 2;
-  static constexpr int MAX_CB = 2;
+  static constexpr int MAX_CB = AU8 ? 1 : 2;
   static constexpr uint32_t STAGE = MAX_CB * WIN_BYTES + B_BYTES;  // 1 KB multiple
   static constexpr uint32_t ZERO = 8192;                           // the all-zero atom
-  static constexpr int STAGES = (200 * 1024 - ZERO) / STAGE > 6 ? 6 : (200 * 1024 - ZERO) / STAGE;
+  static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
+  static constexpr int THREADS = 256 + (AU8 ? 32 * kConvWarps : 0);
+  static constexpr int STAGES = (200 * 1024 - ZERO - RAW) / STAGE > 6 ? 6 : (200 * 1024 - ZERO - RAW) / STAGE;
   static constexpr uint32_t TMEM_COLS = (NMT * BN <= 32) ? 32 : (NMT * BN <= 64) ? 64 : (NMT * BN <= 128) ? 128
                                         : (NMT * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + RAW + 1024 + 256;
   static_assert(NMT * BN <= 512, "TMEM");
 };
 
-template <int BN, int BSWZ, int NMT>
-__global__ void __launch_bounds__(256, 1)
+template <int BN, int BSWZ, int NMT, int AU8 = 0>
+__global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
     umma_wgrad_win_kernel(const __grid_constant__ WgArgs g, const __grid_constant__ CUtensorMap tmX,
                           const __grid_constant__ CUtensorMap tmY) {
-  using C = WgCfg<BN, BSWZ, NMT>;
+  using C = WgCfg<BN, BSWZ, NMT, AU8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                           // stages: [windows | dY box]
   uint8_t* zero = ring + C::STAGES * C::STAGE;    // all-zero atom (above the ring: LBO > 0)
-  uint64_t* full = reinterpret_cast<uint64_t*>(zero + C::ZERO);
+  uint8_t* rawr = zero + C::ZERO;                 // AU8 raw u8 stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(rawr + C::RAW);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* raw_full = tfull + 2;
+  uint64_t* raw_empty = raw_full + kRawStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < (int)(C::ZERO / 16); i += blockDim.x)
     reinterpret_cast<uint4*>(zero)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -739,10 +758,16 @@ __global__ void __launch_bounds__(256, 1)
     sm100::tma_prefetch_desc(&tmX);
     sm100::tma_prefetch_desc(&tmY);
     for (int s = 0; s < C::STAGES; ++s) {
-      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&full[s], AU8 ? 1 + kConvWarps : 1);  // AU8: + one arrival per converter warp
       sm100::mbar_init(&empty[s], 1);
     }
     sm100::mbar_init(tfull, 1);
+    if constexpr (AU8 > 0) {
+      for (int s = 0; s < kRawStages; ++s) {
+        sm100::mbar_init(&raw_full[s], 1);
+        sm100::mbar_init(&raw_empty[s], kConvWarps);
+      }
+    }
     sm100::fence_barrier_init();
   }
   if (warp == 2) sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -750,20 +775,26 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t stage_tx = g.a_cb * g.win_rows * 128 + C::B_BYTES;
+  const uint32_t stage_tx = (AU8 ? 0 : g.a_cb * g.win_rows * 128) + C::B_BYTES;
 
   if (warp == 0) {
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, rs = 0;
+    uint32_t phase = 0, rph = 0;
     for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
       const int kb0 = sp * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
+        if constexpr (AU8 > 0) {  // raw frame lines of the window (converters build it)
+          sm100::mbar_wait(&raw_empty[rs], rph ^ 1);
+          u8_stage_issue(g, (long long)kb * 64 + g.min_off, g.win_rows, rawr + rs * kRawBytes, &raw_full[rs], lane);
+          if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+        }
         sm100::mbar_wait(&empty[stage], phase ^ 1);
         if (sm100::elect_one()) {
           uint8_t* st = ring + stage * C::STAGE;
           sm100::mbar_arrive_expect_tx(&full[stage], stage_tx);
-          for (int cb = 0; cb < g.a_cb; ++cb)
-            sm100::tma_load_2d(st + cb * C::WIN_BYTES, &tmX, &full[stage], cb * 64, kb * 64 + g.min_off);
+          if constexpr (AU8 == 0)
+            for (int cb = 0; cb < g.a_cb; ++cb)
+              sm100::tma_load_2d(st + cb * C::WIN_BYTES, &tmX, &full[stage], cb * 64, kb * 64 + g.min_off);
           uint8_t* sb = st + C::MAX_CB * C::WIN_BYTES;
           if constexpr (BSWZ == 64) {
             sm100::tma_load_2d(sb, &tmY, &full[stage], 0, kb * 64);
@@ -827,7 +858,29 @@ __global__ void __launch_bounds__(256, 1)
       if (sm100::elect_one()) sm100::umma_commit(tfull);
       __syncwarp();
     }
-  } else if (warp >= 4) {
+  } else if (AU8 > 0 && warp >= 8) {
+    // converters: raw stage -> swizzled bf16 window of the stage (then one arrival per warp)
+    const int c = threadIdx.x - 256;
+    int stage = 0, rs = 0;
+    uint32_t phase = 0, rph = 0;
+    for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
+      const int kb0 = sp * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&raw_full[rs], rph);
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        u8_stage_convert(g, (long long)kb * 64 + g.min_off, g.win_rows, rawr + rs * kRawBytes,
+                         ring + stage * C::STAGE, c, 0);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> UMMA reads
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          sm100::mbar_arrive(&full[stage]);
+          sm100::mbar_arrive(&raw_empty[rs]);
+        }
+        if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     const int ew = warp - 4;
     int ti = 0;
     for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x, ++ti) {
