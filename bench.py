@@ -111,6 +111,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def load_traffic():
+    """DRAM bytes per launch of the roofline kernels, from the latest committed ncu captures
+    (profiles/rNN/traffic.json, written by the round's profiling pass); {} if absent."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
+                                          "traffic.json")))
+    if not paths:
+        return {}
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    d["_path"] = os.path.relpath(paths[-1], os.path.dirname(os.path.abspath(__file__)))
+    return d
+
+
 def make_batch(T, B, A, device, seed):
     g = torch.Generator(device=device).manual_seed(seed)
     t1 = T + 1
@@ -436,16 +451,19 @@ def main():
     dominant = max(("forward", "backward"), key=lambda k: br[k])
     dom_flops = fwd_flops if dominant == "forward" else bwd_flops
     achieved = dom_flops / br[dominant] / 1e12
+    tr = load_traffic()
     roofline = {"bound": "tensor", "kernel": f"atari_{dominant} (tcgen05 GEMMs + epilogues)",
                 "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16"], "traffic": None, "peak_kind": pk["kind"],
-                "phase_seconds": br, "flops_per_launch": dom_flops}
+                "frac": achieved / pk["bf16"], "traffic": tr.get(f"atari_{dominant}_cfg1_step"),
+                "traffic_unit": "bytes per step (DRAM read+write, ncu)", "traffic_source": tr.get("_path"),
+                "peak_kind": pk["kind"], "phase_seconds": br, "flops_per_launch": dom_flops}
     timer = kernel_bench.Timer()
     vt = kernel_bench.bench_vtrace(80, 4096, 18, timer, iters=20)
     vt_roof = {"bound": "hbm", "kernel": "vtrace_from_logits T=80 B=4096 A=18",
                "achieved": vt["gbs"], "peak": pk["hbm"], "unit": "GB/s",
-               "frac": vt["gbs"] / pk["hbm"], "traffic": None, "bytes": vt["bytes"],
-               "seconds": vt["median_s"]}
+               "frac": vt["gbs"] / pk["hbm"], "traffic": tr.get("vtrace_from_logits_T80_B4096_A18"),
+               "traffic_source": tr.get("_path"), "bytes": vt["bytes"], "seconds": vt["median_s"],
+               "timing": "steady state over rotating HBM-resident input sets (> 2x L2), CUDA events"}
     ll = kernel_bench.bench_loss(T, B, A, timer, iters=20)
     vt_sweep = {}
     for bb in (4096, 16384, 65536):
