@@ -275,7 +275,8 @@ class AtariNet(nn.Module):
                 getattr(self, "_packed_version", None) != self.flat_params._version)
 
     def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
-                         repack: bool | None = None, lstm: dict | None = None, plane_index=None):
+                         repack: bool | None = None, lstm: dict | None = None, plane_index=None,
+                         keep_x0: bool = True):
         """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
 
         Frame-stack dedup: with plane_index (n,4) int32, `frames` is a plane store
@@ -284,7 +285,8 @@ class AtariNet(nn.Module):
         repack=None packs the bf16 mirror only when stale; False trusts it (the fused
         optimiser step keeps it fresh); True always packs.  LSTM nets take
         lstm=dict(T1, B, done u8 (n,), h0, c0 (2,B,H) f32[, hN, cN]); the final state
-        is returned in lstm["hN"], lstm["cN"]."""
+        is returned in lstm["hN"], lstm["cN"].  keep_x0=False (inference without a backward)
+        skips conv1's X0 side output."""
         if plane_index is not None:
             if plane_index.dtype != torch.int32 or plane_index.shape[-1] != 4:
                 raise DimensionError("plane_index must be int32 (n, 4)")
@@ -303,6 +305,7 @@ class AtariNet(nn.Module):
         if baseline is None:
             baseline = torch.empty(n, device=frames.device)
         stream = N.stream_handle(frames.device)
+        b.struct.flags = 0 if (keep_x0 or self.use_lstm) else N.BP_NET_NO_X0
         if self.use_lstm:
             if lstm is None:
                 raise DimensionError("LSTM AtariNet forward needs done / core_state (lstm=...)")
@@ -409,8 +412,8 @@ class AtariNet(nn.Module):
         elif torch.is_grad_enabled():
             logits, baseline = _AtariFunction.apply(self, frames, reward, last_action,
                                                     *self.parameters())
-        else:
-            logits, baseline = self._forward_kernels(frames, reward, last_action)
+        else:  # inference: no backward follows, conv1 skips the X0 side output
+            logits, baseline = self._forward_kernels(frames, reward, last_action, keep_x0=False)
         action = self.sample(logits.detach(), greedy=not self.training)
         return (dict(policy_logits=logits.view(T, B, self.num_actions), baseline=baseline.view(T, B),
                      action=action.view(T, B)), state)

@@ -417,7 +417,9 @@ struct NetPlan {
 static void make_plan(int n, int sms, NetPlan* P, bool win) {
   const long long rows[4] = {(long long)n * 441, (long long)n * 100, (long long)n * 81, n};
   // conv3's 9 taps x 64 channels pad to 5 m-tiles (the 10th atom is the zero atom)
-  const int M[4] = {256, 512, 576, kCoreW};
+  // window mode: conv1 gets one more m-tile (the all-ones atom -> db1 rows, which spares the
+  // conv2 dgrad epilogue its column sums); conv3's 9 taps leave atom 9 free for db3
+  const int M[4] = {win ? 384 : 256, 512, 576, kCoreW};
   const int Ns[4] = {32, 64, 64, 64};
   size_t off = 0;
   for (int i = 0; i < 4; ++i) {
@@ -882,7 +884,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.out = net->d_pre3;
     g.r_img = 81 * 64;
     g.cdiv = 64; g.cq = 7; g.cs1 = 9 * 64; g.cs2 = 64;
-    g.colsum = ws + P.cs_off[2];
+    g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[2];  // window mode: bias from the wgrad ones atom
     if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
   // conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
@@ -905,7 +907,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.out = net->d_pre2;
     g.gh = 9; g.gw = 9; g.vh = 9; g.vw = 9;
     g.r_img = 100 * 64; g.r_y = 10 * 64; g.r_x = 64;
-    g.colsum = ws + P.cs_off[1];
+    g.colsum = ws + P.cs_off[1];  // db2
     if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
@@ -929,7 +931,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.gh = 10; g.gw = 10; g.vh = 10; g.vw = 10;
     g.r_img = 441 * 32; g.r_y = 2 * 21 * 32; g.r_x = 2 * 32;
     g.cdiv = 32; g.cq = 2; g.cs1 = 21 * 32; g.cs2 = 32;
-    g.colsum = ws + P.cs_off[0];
+    g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[0];  // window mode: bias from the wgrad ones atom
     if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
   }
   // weight gradients
@@ -981,12 +983,13 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.win_rows = (64 + mx + 7) & ~7;
     g.Mpad = (int)w.Mpad;
     g.N = w.Npad;
+    g.ones_atom = i == 1 ? -1 : nshifts * (xcols / 64);  // the atom after the taps: bias rows
     g.out = ws + w.off;
     int r;
     if ((r = make_tmap(&ta, X, xrows, xcols, 64, g.win_rows, 128))) return r;
     if (ncols == 32) {
       if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
-      return launch_wgrad_win<32, 64, 2>(g, ta, tb, s);
+      return launch_wgrad_win<32, 64, 3>(g, ta, tb, s);
     }
     if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
     return i == 1 ? launch_wgrad_win<64, 128, 4>(g, ta, tb, s) : launch_wgrad_win<64, 128, 5>(g, ta, tb, s);
@@ -1013,13 +1016,16 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       g.win_rows = (64 + 22 + 7) & ~7;
       g.Mpad = (int)w.Mpad;
       g.N = w.Npad;
+      g.ones_atom = wgrad_window() ? 4 : -1;
       g.out = ws + w.off;
       g.u8 = src->frames;
       g.u8_index = src->plane_index;
       g.u8_planes = src->num_planes;
       g.u8_rows = (long long)n * 441;
       if ((rc = make_tmap(&tb, net->d_pre1, (long long)n * 441, 32, 32, 64, 64))) return rc;
-      if ((rc = launch_wgrad_win<32, 64, 2, 1>(g, tb, tb, s))) return rc;
+      if ((rc = wgrad_window() ? launch_wgrad_win<32, 64, 3, 1>(g, tb, tb, s)
+                               : launch_wgrad_win<32, 64, 2, 1>(g, tb, tb, s)))
+        return rc;
     } else if (wgrad_window()) {
       if ((rc = wgrad_win(0, net->x0, (long long)n * 441, 64, 4, o1, net->d_pre1, 32))) return rc;
     } else if ((rc = wgrad(0, net->x0, (long long)n * 441, 64, 1, 4, o1, net->d_pre1, 32))) {
@@ -1069,12 +1075,23 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       const WgPlan& w = P.wg[3];
       f.job[k++] = {ws + w.off, nullptr, 2, w.splits, 513 + A + 1, A + 1, w.Npad, w.Mpad, 1.f};
     }
-    // biases: db1 from conv2 dgrad (width 128 = 4 groups of 32), db2, db3 (3136 = 49 x 64), dbfc
+    // biases.  Window mode: db1 and db3 are the all-ones-atom rows of the conv1 / conv3
+    // weight-gradient partials (sums over rows of the bf16 dY), split-reduced like the weights;
+    // db2 and dbfc come from the conv3 / heads dgrad epilogue column sums.  Per-tap mode: db1 from conv2 dgrad (width 128 = 4 groups of 32), db2, db3
+    // (3136 = 49 x 64), dbfc from their epilogue column sums.
     const int pb[4] = {P_B1, P_B2, P_B3, P_BFC};
     const int C[4] = {32, 64, 64, 512};
-    for (int i = 0; i < 4; ++i)
-      f.job[k++] = {ws + P.cs_off[i], grads + off[pb[i]], 1, P.cs_rows[i], P.cs_n[i] / C[i], C[i], 0, 0,
-                    1.f};
+    const int ones_row[3] = {4 * 64, 0, 9 * 64};
+    for (int i = 0; i < 4; ++i) {
+      if ((i == 0 || i == 2) && wgrad_window()) {
+        const WgPlan& w = P.wg[i];
+        f.job[k++] = {ws + w.off + (size_t)ones_row[i] * w.Npad, grads + off[pb[i]], 0, w.splits, 1, C[i],
+                      w.Npad, w.Mpad, 1.f};
+      } else {
+        f.job[k++] = {ws + P.cs_off[i], grads + off[pb[i]], 1, P.cs_rows[i], P.cs_n[i] / C[i], C[i], 0, 0,
+                      1.f};
+      }
+    }
     f.njobs = k;
     f.A = A;
     f.wp_grad = grads + off[P_WP];

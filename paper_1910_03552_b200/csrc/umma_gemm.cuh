@@ -707,6 +707,8 @@ struct WgArgs {
   int row_off[kMaxShifts];        // per-tap row offset (>= 0)
   int min_off, win_rows;          // window rows (multiple of 8)
   int Mpad, N;
+  int ones_atom;  // atom index holding all ones (its D rows = column sums of dY: the bias
+                  // gradient), -1 = none; atoms past the taps and the ones atom are zero
   float* out;
   unsigned long long* trace;
   int trace_tiles;
@@ -725,12 +727,13 @@ struct WgCfg {
   static constexpr int MAX_CB = AU8 ? 1 : 2;
   static constexpr uint32_t STAGE = MAX_CB * WIN_BYTES + B_BYTES;  // 1 KB multiple
   static constexpr uint32_t ZERO = 8192;                           // the all-zero atom
+  static constexpr uint32_t ONES = 8192;                           // the all-ones atom
   static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
   static constexpr int THREADS = 256 + (AU8 ? 32 * kConvWarps : 0);
-  static constexpr int STAGES = (200 * 1024 - ZERO - RAW) / STAGE > 6 ? 6 : (200 * 1024 - ZERO - RAW) / STAGE;
+  static constexpr int STAGES = (200 * 1024 - ZERO - ONES - RAW) / STAGE > 6 ? 6 : (200 * 1024 - ZERO - ONES - RAW) / STAGE;
   static constexpr uint32_t TMEM_COLS = (NMT * BN <= 32) ? 32 : (NMT * BN <= 64) ? 64 : (NMT * BN <= 128) ? 128
                                         : (NMT * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + RAW + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + ONES + RAW + 1024 + 256;
   static_assert(NMT * BN <= 512, "TMEM");
 };
 
@@ -742,7 +745,9 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                           // stages: [windows | dY box]
-  uint8_t* zero = ring + C::STAGES * C::STAGE;    // all-zero atom (above the ring: LBO > 0)
+  // fixed atoms above the ring, ones below zero, so every atom pair has LBO > 0
+  uint8_t* ones = ring + C::STAGES * C::STAGE;    // all-ones atom (bf16 1.0)
+  uint8_t* zero = ones + C::ONES;                 // all-zero atom
   uint8_t* rawr = zero + C::ZERO;                 // AU8 raw u8 stages
   uint64_t* full = reinterpret_cast<uint64_t*>(rawr + C::RAW);
   uint64_t* empty = full + C::STAGES;
@@ -753,6 +758,8 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < (int)(C::ZERO / 16); i += blockDim.x)
     reinterpret_cast<uint4*>(zero)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = threadIdx.x; i < (int)(C::ONES / 16); i += blockDim.x)
+    reinterpret_cast<uint4*>(ones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch_desc(&tmX);
@@ -812,22 +819,24 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
     const uint64_t b_hi = BSWZ == 64 ? sm100::smem_desc(0, 16, 512, sm100::SWZ_64B)
                                      : sm100::smem_desc(0, 8192, 1024, sm100::SWZ_128B);
     constexpr uint32_t b_kstep = BSWZ == 64 ? 1024 : 2048;
-    // per m-tile: A start offset (within a stage; bit 31 = the zero atom) and LBO
-    uint32_t a_off[NMT], a_lbo[NMT];
-    const uint32_t zero_addr = sm100::smem_addr(zero);
+    // per m-tile: the two atoms' addresses.  Window atoms are stage-relative offsets; the
+    // zero / ones atoms are fixed shared addresses above the ring (flag bit 31)
+    constexpr uint32_t kFixed = 0x80000000u;
+    uint32_t a0[NMT], a1[NMT];
+    const uint32_t zero_addr = sm100::smem_addr(zero), ones_addr = sm100::smem_addr(ones);
 #pragma unroll
     for (int mt = 0; mt < NMT; ++mt) {
       uint32_t ad[2];
-      bool z[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int atom = 2 * mt + j;
         const int sft = atom / g.atoms_per_shift, cb = atom - sft * g.atoms_per_shift;
-        z[j] = sft >= g.nshifts;
-        ad[j] = z[j] ? 0u : cb * C::WIN_BYTES + (uint32_t)(g.row_off[sft] - g.min_off) * 128u;
+        if (atom == g.ones_atom) ad[j] = kFixed | ones_addr;
+        else if (sft >= g.nshifts) ad[j] = kFixed | zero_addr;
+        else ad[j] = cb * C::WIN_BYTES + (uint32_t)(g.row_off[sft] - g.min_off) * 128u;
       }
-      a_off[mt] = ad[0];
-      a_lbo[mt] = z[1] ? 0xffffffffu : ad[1] - ad[0];  // zero atom: resolved per stage below
+      a0[mt] = ad[0];
+      a1[mt] = ad[1];
     }
     // one K range (split) per CTA: grid == splits (single accumulator set)
     int stage = 0;
@@ -842,8 +851,9 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
         if (sm100::elect_one()) {
 #pragma unroll
           for (int mt = 0; mt < NMT; ++mt) {
-            const uint32_t sa = st + a_off[mt];
-            const uint32_t lbo = a_lbo[mt] == 0xffffffffu ? zero_addr - sa : a_lbo[mt];
+            const uint32_t sa = (a0[mt] & kFixed) ? (a0[mt] & ~kFixed) : st + a0[mt];
+            const uint32_t sb1 = (a1[mt] & kFixed) ? (a1[mt] & ~kFixed) : st + a1[mt];
+            const uint32_t lbo = sb1 - sa;  // the second atom is above the first (checked on the host)
             const uint64_t a_hi = sm100::smem_desc(0, lbo, 1024, sm100::SWZ_128B);
 #pragma unroll
             for (int k = 0; k < 4; ++k)

@@ -85,7 +85,9 @@ class FusedLearner:
     def _graph_key(self, batch, optimizer):
         keys = (("frame_planes", "frame_index") if "frame_planes" in batch else ("frame",)) + (
             "reward", "done", "policy_logits", "action", "last_action")
-        return tuple(batch[k].data_ptr() for k in keys) + (id(optimizer),)
+        ep = batch.get("episode_return") if isinstance(batch, dict) else None
+        return tuple(batch[k].data_ptr() for k in keys) + (
+            ep.data_ptr() if ep is not None else 0, id(optimizer))
 
     def step(self, batch, optimizer=None, scheduler=None, initial_agent_state=()):
         """Enqueue one learner step on the current stream; returns the device loss vector.
@@ -192,21 +194,31 @@ class FusedLearner:
                 m.flat_grads.mul_(coef)
                 optimizer.step()
                 m.mirror_fresh = False
+        self._pack_stats(batch, self.losses)
         return self.losses
 
-    def stats(self, batch, losses=None):
-        """Upstream learn() stats dict: the loss vector, done[1:] and episode_return[1:]
-        are packed on the device and read back with ONE pinned D2H copy (one sync)."""
+    def _pack_stats(self, batch, losses):
+        """Loss vector, done[1:] and episode_return[1:] -> one device buffer -> ONE pinned D2H
+        copy.  Part of the step (and of its CUDA graph)."""
         T, B = self.T, self.B
         tb = T * B
         dev_buf, host = self._stats_dev, self._stats_host
-        dev_buf[:32].view(torch.float64).copy_(self.losses if losses is None else losses)
+        dev_buf[:32].view(torch.float64).copy_(losses)
         dev_buf[32:32 + tb].copy_(batch["done"][1:].reshape(tb).view(torch.uint8)
                                   if batch["done"].dtype == torch.bool else batch["done"][1:].reshape(tb))
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
         if ep is not None:
             dev_buf[32 + tb:].view(torch.float32).copy_(ep[1:].reshape(tb))
         host.copy_(dev_buf, non_blocking=True)
+
+    def stats(self, batch, losses=None):
+        """Upstream learn() stats dict from the step's packed read-back (one sync)."""
+        T, B = self.T, self.B
+        tb = T * B
+        host = self._stats_host
+        if losses is not None:  # an explicit loss vector: pack it now
+            self._pack_stats(batch, losses)
+        ep = batch.get("episode_return") if isinstance(batch, dict) else None
         self._stats_event.record()
         self._stats_event.synchronize()
         pg, base, ent, total = host[:32].view(torch.float64).tolist()
