@@ -399,7 +399,7 @@ def main():
                 infeed.release()
             return out
 
-        e2e_run(2)
+        e2e_run(6)  # per infeed slot: eager step, graph capture, replay -> timed steps replay only
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
