@@ -43,7 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_forward": (I, [P, I, P, P, P, P, P, P, P]),
     "bp_atari_set_conv1_u8": (I, [I]),
     "bp_atari_set_wgrad_window": (I, [I]),
-    "bp_gemm_trace_next": (I, [P, I]),
+    "bp_gemm_trace_next": (I, [P, I, I]),
     "bp_atari_forward_planes": (I, [P, I, P, P, I, P, P, P, P, P, P]),
     "bp_atari_backward": (I, [P, I, P, P, P, P, P, P]),
     "bp_atari_backward_frames": (I, [P, I, P, P, I, P, P, P, P]),

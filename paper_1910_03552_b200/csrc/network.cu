@@ -120,7 +120,7 @@ static bool wgrad_window() {
 }
 
 static void* g_trace_next = nullptr;
-static int g_trace_tiles = 0;
+static int g_trace_tiles = 0, g_trace_skip = 0;
 
 template <int BN, int BSWZ, int NMT, int AU8 = 0>
 static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUtensorMap& ty, cudaStream_t s) {
@@ -148,10 +148,15 @@ static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensor
   GemmArgs g = g0;
   gemm_prepare(g);
 
+
   if (g_trace_next) {  // debug: per-tile role timeline of this launch (bp_gemm_trace_next)
-    g.trace = reinterpret_cast<unsigned long long*>(g_trace_next);
-    g.trace_tiles = g_trace_tiles;
-    g_trace_next = nullptr;
+    if (g_trace_skip > 0) {
+      --g_trace_skip;
+    } else {
+      g.trace = reinterpret_cast<unsigned long long*>(g_trace_next);
+      g.trace_tiles = g_trace_tiles;
+      g_trace_next = nullptr;
+    }
   }
   using Cfg = GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>;
   auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW, AU8>;
@@ -569,9 +574,10 @@ extern "C" int bp_gemm_shift_test(const void* A, const void* B, float* Cout, int
 
 // debug: the next GEMM launch records per-tile role timestamps (%globaltimer ns) into
 // buf[(cta * tiles + i) * 16 + event] (0/1 producer, 2/3 MMA, 4/5 epilogue, 6/7 u8 converter)
-extern "C" int bp_gemm_trace_next(void* buf, int tiles) {
+extern "C" int bp_gemm_trace_next(void* buf, int tiles, int skip) {
   g_trace_next = buf;
   g_trace_tiles = tiles;
+  g_trace_skip = skip;
   return BP_OK;
 }
 

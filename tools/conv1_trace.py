@@ -9,6 +9,7 @@ sys.path.insert(0, ".")
 from paper_1910_03552_b200 import _native as N  # noqa: E402
 from paper_1910_03552_b200.atari_net import AtariNet  # noqa: E402
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # 0 conv1, 1 conv2, 2 conv3, 3 fc, 4 heads
 N.lib().bp_atari_set_conv1_u8(mode)
 n = 2592
 net = AtariNet(num_actions=6)
@@ -19,15 +20,16 @@ TT = 80
 tr = torch.zeros(148 * TT * 16, dtype=torch.int64, device="cuda")
 for it in range(3):
     if it == 2:
-        N.lib().bp_gemm_trace_next(tr.data_ptr(), TT)
+        N.lib().bp_gemm_trace_next(tr.data_ptr(), TT, skip)
     net._forward_kernels(frames, rew, la, repack=True)
 torch.cuda.synchronize()
 t = tr.view(148, TT, 16).cpu().numpy().astype(np.float64)
-ntiles = (n * 441 + 127) // 128
+ntiles = [(n * 441 + 127) // 128, (n * 100 + 127) // 128, (n * 81 + 127) // 128,
+          ((n + 127) // 128) * 8, (n + 127) // 128][skip]
 per = [len(range(b, ntiles, 148)) for b in range(148)]
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan)
-print(f"== conv1 u8={mode}: tiles/CTA {per[0]}, kernel span {np.nanmax(t)/1e3:.1f} us")
+print(f"== gemm #{skip} u8={mode}: tiles/CTA {per[0]}, kernel span {np.nanmax(t)/1e3:.1f} us")
 b = 0
 for i in list(range(min(per[b], 6))) + list(range(max(6, per[b] - 3), per[b])):
     e = t[b, i]
