@@ -107,8 +107,8 @@ struct FwdSmem {
   __nv_bfloat16 in[2][CS][NB][SL];       // incoming slices: [parity][source CTA][batch][unit]
   __nv_bfloat16 out[NB][SL];             // this CTA's new h slice
   float red[4][MT * 16][NB];             // per K-quarter partial pre-gates
-  float act[NB][5][UC];                  // step outputs staged for the writer warps: i f g o c
-  __nv_bfloat16 hb[2][NB][UC];           // h_t, notdone_t * h_{t-1} (bf16 sequences)
+  float act[2][NB][5][UC];               // step outputs by step parity: i f g o c
+  __nv_bfloat16 hb[2][2][NB][UC];        // h_t, notdone_t * h_{t-1} (bf16 sequences), by parity
   uint64_t bar[2];                       // incoming-slice barriers, by step parity
 };
 
@@ -203,10 +203,35 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
   const int ncols = a.B - cb < NB ? a.B - cb : NB;
   cluster_sync_all();  // every CTA running, barriers initialised, before any DSMEM traffic
   if (trace) trace[4 * a.T1 * 2 + 1] = gtimer();
+  // the outputs of step tt (staged in smem by parity), coalesced along the CTA's 34 units and
+  // written by every thread: issued at the top of step tt + 1, where the stores overlap the
+  // latency-bound recurrent MMAs instead of sitting before the exchange wait
+  auto store_step = [&](int tt) {
+    if (a.dbg & 1) return;
+    const int pp = tt & 1;
+    const size_t trow = (size_t)tt * a.ldb + a.b0 + cb;
+    // one (batch, quantity) segment of the CTA's units per warp: warp-uniform branches
+    for (int sg = warp; sg < ncols * 7; sg += WARPS) {
+      const int b = sg / 7, k = sg - b * 7;
+      const size_t row = trow + b;
+      for (int u = lane; u < nu; u += 32) {
+        if (k < 4) a.gates[row * H4 + (size_t)k * H + u0 + u] = S.act[pp][b][k][u];
+        else if (k == 4) a.cseq[row * H + u0 + u] = S.act[pp][b][4][u];
+        else if (k == 5) a.out_aug[row * a.aug_ld + u0 + u] = S.hb[pp][0][b][u];
+        else a.hprev_aug[row * a.aug_ld + u0 + u] = S.hb[pp][1][b][u];
+      }
+    }
+    if (rank == 0 && tid < ncols) {  // bias (ones) column of both augmented rows
+      const size_t row = trow + tid;
+      a.out_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
+      a.hprev_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
+    }
+  };
 
   for (int t = 0; t < a.T1; ++t) {
     const int p = t & 1;
     if (trace) trace[t * 4 + 0] = gtimer();
+    if (t > 0) store_step(t - 1);
     // ---- recurrent pre-gates W_hh h_{t-1}: 3 independent accumulator chains per warp
     {
       float acc[ITEMS][4];
@@ -258,13 +283,13 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
       const float h = og * tanh_fast(c);
       const __nv_bfloat16 hb = __float2bfloat16_rn(h);
       S.out[ob][ou] = hb;
-      S.act[ob][0][ou] = ig;
-      S.act[ob][1][ou] = fg;
-      S.act[ob][2][ou] = gg;
-      S.act[ob][3][ou] = og;
-      S.act[ob][4][ou] = c;
-      S.hb[0][ob][ou] = hb;
-      S.hb[1][ob][ou] = __float2bfloat16_rn(nd * hown);
+      S.act[p][ob][0][ou] = ig;
+      S.act[p][ob][1][ou] = fg;
+      S.act[p][ob][2][ou] = gg;
+      S.act[p][ob][3][ou] = og;
+      S.act[p][ob][4][ou] = c;
+      S.hb[p][0][ob][ou] = hb;
+      S.hb[p][1][ob][ou] = __float2bfloat16_rn(nd * hown);
       hown = h;
       if (t == a.T1 - 1) {
         a.hN[(size_t)(a.b0 + col) * H + j] = h;
@@ -284,26 +309,6 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
         bulk_commit();
       }
     }
-    // ---- the step's outputs, coalesced along the CTA's 34 units, written by every thread
-    //      while the slices travel (off the recurrent critical path)
-    if (!(a.dbg & 1)) {
-      const size_t trow = (size_t)t * a.ldb + a.b0 + cb;
-      for (int e = tid; e < ncols * 7 * UC; e += THREADS) {
-        const int b = e / (7 * UC), rem = e % (7 * UC);
-        const int k = rem / UC, u = rem % UC;
-        if (u >= nu) continue;
-        const size_t row = trow + b;
-        if (k < 4) a.gates[row * H4 + (size_t)k * H + u0 + u] = S.act[b][k][u];
-        else if (k == 4) a.cseq[row * H + u0 + u] = S.act[b][4][u];
-        else if (k == 5) a.out_aug[row * a.aug_ld + u0 + u] = S.hb[0][b][u];
-        else a.hprev_aug[row * a.aug_ld + u0 + u] = S.hb[1][b][u];
-      }
-      if (rank == 0 && tid < ncols) {  // bias (ones) column of both augmented rows
-        const size_t row = trow + tid;
-        a.out_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
-        a.hprev_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
-      }
-    }
     if (!exch) break;
     mbar_wait_parity(&S.bar[p], phase[p]);
     phase[p] ^= 1u;
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
     __syncthreads();
     if (trace) trace[t * 4 + 3] = gtimer();
   }
+  store_step(a.T1 - 1);
   if (tid < CS) bulk_wait_read_all();
   cluster_sync_all();  // no CTA leaves while a peer may still read / write its shared memory
 }
