@@ -238,11 +238,25 @@ __global__ void __launch_bounds__(128) frames_s2d_kernel(const uint8_t* __restri
   }
 }
 
-// Augmented core columns 512..575 of every frame: [clip(reward), onehot(last_action) (A),
-// 1 (bias), 0 ...] (the frames_s2d_kernel side job, for the u8 conv1 path)
-__global__ void core_aug_kernel(const float* __restrict__ reward, const int64_t* __restrict__ last_action,
-                                __nv_bfloat16* __restrict__ core, int n, int A) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// one launch for the forward's two small jobs: blocks [0, 36) pack the heads operand, the
+// rest write the augmented core columns (u8 conv1 path)
+__global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp, const float* __restrict__ bp,
+                                                   const float* __restrict__ wv, const float* __restrict__ bv,
+                                                   __nv_bfloat16* __restrict__ whf, const float* __restrict__ reward,
+                                                   const int64_t* __restrict__ last_action,
+                                                   __nv_bfloat16* __restrict__ core, int n, int A) {
+  if (blockIdx.x < 36) {
+    const int core_w = 513 + A;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += 36 * blockDim.x) {
+      const int a = i / kCoreW, j = i % kCoreW;
+      float v = 0.f;
+      if (a < A) v = j < core_w ? wp[(size_t)a * core_w + j] : (j == core_w ? bp[a] : 0.f);
+      else if (a == A) v = j < core_w ? wv[j] : (j == core_w ? bv[0] : 0.f);
+      whf[i] = __float2bfloat16_rn(v);
+    }
+    return;
+  }
+  const long long i = (long long)(blockIdx.x - 36) * blockDim.x + threadIdx.x;
   if (i >= (long long)n * 64) return;
   const long long img = i >> 6;
   const int j = (int)(i & 63);
@@ -288,7 +302,7 @@ __global__ void pack_heads_kernel(const float* __restrict__ wp, const float* __r
                                   const float* __restrict__ wv, const float* __restrict__ bv,
                                   __nv_bfloat16* __restrict__ whf, int A) {
   const int core = 513 + A;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += 36 * blockDim.x) {
     const int a = i / kCoreW, j = i % kCoreW;
     float v = 0.f;
     if (a < A) v = j < core ? wp[(size_t)a * core + j] : (j == core ? bp[a] : 0.f);
@@ -646,16 +660,18 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
   if (conv1_u8()) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
-    core_aug_kernel<<<(n * 64 + 255) / 256, 256, 0, s>>>(reward, last_action, bf(net->core), n, A);
-    if ((rc = check_launch("core_aug_kernel"))) return rc;
+    prep_kernel<<<36 + (n * 64 + 511) / 512, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
+                                                          params + off[P_BV], bf(net->whf), reward, last_action,
+                                                          bf(net->core), n, A);
+    if ((rc = check_launch("prep_kernel"))) return rc;
   } else {
     frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
                                              bf(net->core), A);
     if ((rc = check_launch("frames_s2d_kernel"))) return rc;
+    pack_heads_kernel<<<36, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
+                                         params + off[P_BV], bf(net->whf), A);
+    if ((rc = check_launch("pack_heads_kernel"))) return rc;
   }
-  pack_heads_kernel<<<36, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
-                                       params + off[P_BV], bf(net->whf), A);
-  if ((rc = check_launch("pack_heads_kernel"))) return rc;
   CUtensorMap ta, tb;
   // 2. conv1: X0 [n*441, 64] x W1 [32, 256] -> relu(./255 + b1) -> X1 (s2d-2 layout)
   //    u8 mode: the X0 window of every tile is built on chip from the u8 frames

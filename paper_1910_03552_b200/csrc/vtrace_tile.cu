@@ -467,7 +467,8 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
   }();
   // columns per tile: BT * A * 4 bytes per TMA box row must be a multiple of 16
   // from_logits at large B streams best with 8-column tiles (fewer, longer TMA rows)
-  int kBT = bt_env ? bt_env : (!loss && B >= 16384 && B % 8 == 0) ? 8 : 4;
+  // small B (the per-GPU learner batch) is latency-bound: 2-column tiles double the CTAs
+  int kBT = bt_env ? bt_env : (!loss && B >= 16384 && B % 8 == 0) ? 8 : (B <= 256 && B % 2 == 0) ? 2 : 4;
   if (!(kBT == 2 || kBT == 4 || kBT == 8) || T * kBT > 992) kBT = 4;
   if (!(A == 6 || A == 18) || B % kBT || T > kMaxT || T * kBT > 992) return BP_ERR_UNSUPPORTED;
   const uintptr_t al = reinterpret_cast<uintptr_t>(beh) | reinterpret_cast<uintptr_t>(tgt) |
