@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import threading
 
+import numpy as np
 import torch
 
 from . import _native as N  # noqa: F401  (fail loudly if the library is missing)
@@ -62,6 +63,12 @@ class FusedLearner:
                                        pin_memory=True)
         self._stats_dev = torch.empty_like(self._stats_host, device=dev)
         self._stats_event = torch.cuda.Event()
+        # numpy views of the pinned read-back buffer (no per-step tensor/numpy conversions)
+        tb = unroll_length * batch_size
+        hnp = self._stats_host.numpy()
+        self._np_losses = hnp[:32].view(np.float64)
+        self._np_done = hnp[32:32 + tb].view(np.bool_)
+        self._np_ret = hnp[32 + tb:].view(np.float32)
         self.pg = process_group
         model.buffers_for(self.n)
         # LSTM core: the initial agent state is staged into fixed buffers (graph inputs)
@@ -213,24 +220,17 @@ class FusedLearner:
 
     def stats(self, batch, losses=None):
         """Upstream learn() stats dict from the step's packed read-back (one sync)."""
-        T, B = self.T, self.B
-        tb = T * B
-        host = self._stats_host
         if losses is not None:  # an explicit loss vector: pack it now
             self._pack_stats(batch, losses)
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
         self._stats_event.record()
         self._stats_event.synchronize()
-        pg, base, ent, total = host[:32].view(torch.float64).tolist()
+        pg, base, ent, total = self._np_losses.tolist()
         cfg = self.cfg
-        if ep is not None:
-            done = host[32:32 + tb].numpy().astype(bool)
-            returns = torch.from_numpy(host[32 + tb:].view(torch.float32).numpy()[done].copy())
-        else:
-            returns = torch.zeros(0)
+        returns = self._np_ret[self._np_done] if ep is not None else self._np_ret[:0]
         return {
-            "episode_returns": tuple(returns.numpy()),
-            "mean_episode_return": float(returns.mean()) if returns.numel() else float("nan"),
+            "episode_returns": tuple(returns.tolist()),
+            "mean_episode_return": float(returns.mean()) if returns.size else float("nan"),
             "total_loss": total,
             "pg_loss": pg * cfg.pg_cost,
             "baseline_loss": base * cfg.baseline_cost,
