@@ -757,11 +757,15 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   }
   // 5. fc: X3 [n, 3136] x Wfc [512, 3136] -> core[:, :512] = relu(. + bfc)
   {
+    // 128-column tiles when 64-column ones would need a second wave: half the re-reads of
+    // X3 from L2 (the fc GEMM is L2->SM bandwidth-bound) and a single wave
+    const int mt = (n + 127) / 128;
+    const bool wide = mt * 8 > g_num_sms;
     if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 128, 128))) return rc;
-    if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, wide ? 128 : 64, 128))) return rc;
     GemmArgs g = base_args();
-    g.m_tiles = (n + 127) / 128;
-    g.n_tiles = 8;
+    g.m_tiles = mt;
+    g.n_tiles = wide ? 4 : 8;
     g.num_kb = g.kb_per_split = 49;
     g.a_cb = 49;
     g.N = 512;
@@ -771,7 +775,9 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.out = net->core;
     g.bits_out = reinterpret_cast<uint32_t*>(net->mc);
     g.r_img = kCoreW;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = wide ? launch_gemm<128, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s)
+                   : launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s)))
+      return rc;
   }
   return BP_OK;
 }
@@ -907,7 +913,12 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.r_img = 81 * 64;
     g.cdiv = 64; g.cq = 7; g.cs1 = 9 * 64; g.cs2 = 64;
     g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[2];  // window mode: bias from the wgrad ones atom
-    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    if (wgrad_window()) {  // 128-column tiles (the last half empty): d_fc re-read 25x instead of 49x
+      g.n_tiles = 25;
+      if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    } else if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) {
+      return rc;
+    }
   }
   // conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
   {
@@ -1063,22 +1074,28 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     const int o0[1] = {0};
     if ((rc = wgrad(3, head_in, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
   }
-  // fc weight gradient with swapped roles: D[o][k] = sum_n d_fc[n][o] X3[n][k] -> grads, no split
+  // fc weight gradient, transposed: D[k][o] = sum_n X3[n][k] d_fc[n][o] (M = 3136 features in 25
+  // m-tiles, N = 512 in 128-column tiles: one wave of 100 tiles, X3 read 4x / d_fc 25x from L2),
+  // stored transposed into grads[o][k] (per column, a warp's 32 rows are one contiguous run)
   {
-    if ((rc = make_tmap(&ta, net->d_fc, n, 512, 64, 64, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->x3, n, 3136, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, net->d_fc, n, 512, 64, 64, 128))) return rc;
     GemmArgs g = base_args();
-    g.m_tiles = 4;
-    g.n_tiles = 49;
+    g.m_tiles = (3136 + 127) / 128;
+    g.n_tiles = 4;
     g.num_kb = g.kb_per_split = (n + 63) / 64;
-    g.a_atoms_per_shift = 8;
+    g.a_atoms_per_shift = 49;
     g.a_nshifts = 1;
-    g.N = 3136;
-    g.M = 512;
+    g.N = 512;
+    g.M = 3136;
     g.out_f32 = 1;
     g.out = grads + off[P_WFC];
-    g.r_img = 3136;
-    if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    g.r_img = 1;
+    g.cdiv = 1;
+    g.cq = 1;
+    g.cs1 = 3136;
+    g.col_stride = 3136;
+    if ((rc = launch_gemm<128, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
   // deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
   {

@@ -97,6 +97,7 @@ struct GemmArgs {
                              // as X0 [rows][64] bf16 (the conv1 weight-gradient operand)
   // epilogue divisors (filled by the launcher from gh*gw, gw, sy, sx, cdiv, cq)
   FDiv fd_per, fd_gw, fd_sy, fd_sx, fd_cdiv, fd_cq, fd_splits, fd_ntiles;
+  long long col_stride;  // f32 output only: element stride between consecutive columns (0 = 1, vector stores)
 };
 
 inline void gemm_prepare(GemmArgs& g) {
@@ -237,6 +238,7 @@ BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
                               int sp, int mt, int ew, int lane, float (&v)[32], uint32_t mkw,
                               float* csum_acc) {
+  if (n0 >= g.N) return;  // a partial last column tile (warp-uniform)
   if (g.heads) {
     if (row_ok) {
 #pragma unroll
@@ -283,7 +285,11 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
       for (int i = 0; i < 32; ++i) bits |= (v[i] > 0.f ? 1u : 0u) << i;
       g.bits_out[off >> 5] = bits;
     }
-    if (g.out_f32) {
+    if (g.out_f32 && g.col_stride) {  // transposed store: per column, the warp's 32 rows are contiguous
+      float* o = reinterpret_cast<float*>(g.out) + off;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[(long long)i * g.col_stride] = v[i];
+    } else if (g.out_f32) {
       float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -644,10 +650,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;
       if (g.mask_bits && row_ok) {
         const uint32_t* mp = g.mask_bits + (((size_t)m * (g.mask_ld ? g.mask_ld : g.N) + nt * BN) >> 5);
+        const int nc = nt * BN;  // only the chunks inside N (a partial last column tile)
         mk0 = __ldg(mp);
-        if (NCH > 1) mk1 = __ldg(mp + 1);
-        if (NCH > 2) mk2 = __ldg(mp + 2);
-        if (NCH > 3) mk3 = __ldg(mp + 3);
+        if (NCH > 1 && nc + 32 < g.N) mk1 = __ldg(mp + 1);
+        if (NCH > 2 && nc + 64 < g.N) mk2 = __ldg(mp + 2);
+        if (NCH > 3 && nc + 96 < g.N) mk3 = __ldg(mp + 3);
       }
       sm100::mbar_wait(&tfull[acc], aphase);
       sm100::tc_fence_after();
