@@ -122,12 +122,12 @@ static bool wgrad_window() {
 static void* g_trace_next = nullptr;
 static int g_trace_tiles = 0, g_trace_skip = 0;
 
-template <int BN, int BSWZ, int NMT, int AU8 = 0>
+template <int BN, int BSWZ, int NMT, int AU8 = 0, int CB = 1, int WR = 88>
 static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUtensorMap& ty, cudaStream_t s) {
-  using Cfg = WgCfg<BN, BSWZ, NMT, AU8>;
-  auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT, AU8>;
+  using Cfg = WgCfg<BN, BSWZ, NMT, AU8, CB, WR>;
+  auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT, AU8, CB, WR>;
   WgArgs g = g0;
-  if (g.win_rows > 160 || g.a_cb > Cfg::MAX_CB || g.splits < 1) {
+  if (g.win_rows > WR || g.a_cb > Cfg::MAX_CB || g.splits < 1) {
     set_error("wgrad window: %d rows / %d channel blocks unsupported", g.win_rows, g.a_cb);
     return BP_ERR_ARG;
   }
@@ -1022,10 +1022,11 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     if ((r = make_tmap(&ta, X, xrows, xcols, 64, g.win_rows, 128))) return r;
     if (ncols == 32) {
       if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
-      return launch_wgrad_win<32, 64, 3>(g, ta, tb, s);
+      return launch_wgrad_win<32, 64, 3, 0, 1, 88>(g, ta, tb, s);
     }
     if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
-    return i == 1 ? launch_wgrad_win<64, 128, 4>(g, ta, tb, s) : launch_wgrad_win<64, 128, 5>(g, ta, tb, s);
+    return i == 1 ? launch_wgrad_win<64, 128, 4, 0, 2, 80>(g, ta, tb, s)
+                  : launch_wgrad_win<64, 128, 5, 0, 1, 88>(g, ta, tb, s);
   };
   {
     const int o1[4] = {0, 1, 21, 22};
@@ -1056,8 +1057,8 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       g.u8_planes = src->num_planes;
       g.u8_rows = (long long)n * 441;
       if ((rc = make_tmap(&tb, net->d_pre1, (long long)n * 441, 32, 32, 64, 64))) return rc;
-      if ((rc = wgrad_window() ? launch_wgrad_win<32, 64, 3, 1>(g, tb, tb, s)
-                               : launch_wgrad_win<32, 64, 2, 1>(g, tb, tb, s)))
+      if ((rc = wgrad_window() ? launch_wgrad_win<32, 64, 3, 1, 1, 88>(g, tb, tb, s)
+                               : launch_wgrad_win<32, 64, 2, 1, 1, 88>(g, tb, tb, s)))
         return rc;
     } else if (wgrad_window()) {
       if ((rc = wgrad_win(0, net->x0, (long long)n * 441, 64, 4, o1, net->d_pre1, 32))) return rc;

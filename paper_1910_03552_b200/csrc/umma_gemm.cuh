@@ -727,28 +727,31 @@ struct WgArgs {
   __nv_bfloat16* u8_x0_out;  // (unused here)
 };
 
-template <int BN, int BSWZ, int NMT, int AU8 = 0>
+// CB: 64-channel blocks of X (windows per stage); WR: window rows (multiple of 8), sized per
+// conv so that the stage ring holds as many K-blocks in flight as shared memory allows
+template <int BN, int BSWZ, int NMT, int AU8 = 0, int CB = 1, int WR = 88>
 struct WgCfg {
-  static constexpr uint32_t WIN_BYTES = 160 * 128;  // <= 160 window rows per channel block
+  static_assert(WR % 8 == 0 && WR <= 160, "window rows");
+  static constexpr uint32_t WIN_BYTES = WR * 128;   // one window per channel block
   static constexpr uint32_t B_BYTES = BN * 64 * 2;
-  static constexpr int MAX_CB = AU8 ? 1 : 2;
+  static constexpr int MAX_CB = CB;
   static constexpr uint32_t STAGE = MAX_CB * WIN_BYTES + B_BYTES;  // 1 KB multiple
   static constexpr uint32_t ZERO = 8192;                           // the all-zero atom
   static constexpr uint32_t ONES = 8192;                           // the all-ones atom
   static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
   static constexpr int THREADS = 256 + (AU8 ? 32 * kConvWarps : 0);
-  static constexpr int STAGES = (200 * 1024 - ZERO - ONES - RAW) / STAGE > 6 ? 6 : (200 * 1024 - ZERO - ONES - RAW) / STAGE;
+  static constexpr int STAGES = (200 * 1024 - ZERO - ONES - RAW) / STAGE > 12 ? 12 : (200 * 1024 - ZERO - ONES - RAW) / STAGE;
   static constexpr uint32_t TMEM_COLS = (NMT * BN <= 32) ? 32 : (NMT * BN <= 64) ? 64 : (NMT * BN <= 128) ? 128
                                         : (NMT * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + ONES + RAW + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + ZERO + ONES + RAW + 1024 + 512;
   static_assert(NMT * BN <= 512, "TMEM");
 };
 
-template <int BN, int BSWZ, int NMT, int AU8 = 0>
-__global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8>::THREADS, 1)
+template <int BN, int BSWZ, int NMT, int AU8 = 0, int CB = 1, int WR = 88>
+__global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
     umma_wgrad_win_kernel(const __grid_constant__ WgArgs g, const __grid_constant__ CUtensorMap tmX,
                           const __grid_constant__ CUtensorMap tmY) {
-  using C = WgCfg<BN, BSWZ, NMT, AU8>;
+  using C = WgCfg<BN, BSWZ, NMT, AU8, CB, WR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                           // stages: [windows | dY box]
