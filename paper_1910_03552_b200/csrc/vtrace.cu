@@ -38,12 +38,7 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
                float baseline_cost, float entropy_cost, int reward_clip, float* vs, float* pg,
                float* log_rhos, float* beh_logp, float* tgt_logp, float* d_logits, float* d_baseline,
                double* losses, void* workspace, size_t ws_bytes, unsigned* status, cudaStream_t s);
-int vt2_launch(bool loss, const float* beh, const float* tgt, const int64_t* act, const void* disc_or_done,
-               const float* rew, const float* val, const float* boot, int T, int B, int A,
-               float clip_rho, float clip_pg_rho, float clip_c, float discount, float pg_cost,
-               float baseline_cost, float entropy_cost, int reward_clip, float* vs, float* pg,
-               float* log_rhos, float* beh_logp, float* tgt_logp, float* d_logits, float* d_baseline,
-               double* losses, void* workspace, size_t ws_bytes, unsigned* status, cudaStream_t s);
+
 
 enum { MODE_LOGITS = 0, MODE_IW = 1, MODE_LOSS = 2 };
 
@@ -659,14 +654,8 @@ extern "C" int bp_vtrace_from_logits_f32(const float* behavior_logits, const flo
   a.beh_logp = behavior_logp;
   a.tgt_logp = target_logp;
   a.status = status;
-  // bandwidth regime: tile-resident kernel (vtrace_tile.cu), then the persistent
-  // TMA producer/consumer kernel (vtrace_tma.cu)
-  int rc = vt3_launch(false, behavior_logits, target_logits, actions, discounts, rewards, values,
-                      bootstrap_value, T, B, A, clip_rho, clip_pg_rho, clip_c, 0.f, 0.f, 0.f, 0.f, 0,
-                      vs, pg_advantages, log_rhos, behavior_logp, target_logp, nullptr, nullptr,
-                      nullptr, nullptr, 0, status, (cudaStream_t)stream);
-  if (rc != BP_ERR_UNSUPPORTED) return rc;
-  rc = vt2_launch(false, behavior_logits, target_logits, actions, discounts, rewards, values,
+  // bandwidth regime: tile-resident kernel (vtrace_tile.cu); other shapes: the generic kernel
+  const int rc = vt3_launch(false, behavior_logits, target_logits, actions, discounts, rewards, values,
                             bootstrap_value, T, B, A, clip_rho, clip_pg_rho, clip_c, 0.f, 0.f, 0.f, 0.f, 0,
                             vs, pg_advantages, log_rhos, behavior_logp, target_logp, nullptr, nullptr,
                             nullptr, nullptr, 0, status, (cudaStream_t)stream);
@@ -710,7 +699,7 @@ extern "C" size_t bp_learner_loss_workspace_bytes(int T, int B, int A) {
   (void)A;
   const int bt = pick_bt(B, T);
   const size_t grid = (size_t)(B + bt - 1) / bt;
-  const size_t grid2 = (size_t)(B + 3) / 4;  // persistent kernel: <= min(B/4, 2 x SMs)
+  const size_t grid2 = (size_t)(B + 1) / 2;  // tile-resident kernel: <= B / 2 tiles (2-column tiles)
   return 256 + (grid > grid2 ? grid : grid2) * 3 * sizeof(double);
 }
 
@@ -765,12 +754,6 @@ extern "C" int bp_learner_loss_f32(const float* learner_logits, const float* lea
                         discount, pg_cost, baseline_cost, entropy_cost, reward_clip, vs, pg_advantages,
                         nullptr, nullptr, nullptr, d_logits, d_baseline, losses, workspace,
                         bp_learner_loss_workspace_bytes(T, B, A), status, (cudaStream_t)stream);
-    if (rc != BP_ERR_UNSUPPORTED) return rc;
-    rc = vt2_launch(true, behavior_logits, learner_logits, actions, done, rewards, learner_baseline,
-                              learner_baseline + (size_t)T * B, T, B, A, clip_rho, clip_pg_rho, clip_c,
-                              discount, pg_cost, baseline_cost, entropy_cost, reward_clip, vs, pg_advantages,
-                              nullptr, nullptr, nullptr, d_logits, d_baseline, losses, workspace,
-                              bp_learner_loss_workspace_bytes(T, B, A), status, (cudaStream_t)stream);
     if (rc != BP_ERR_UNSUPPORTED) return rc;
   }
   const bool vec = aligned16(learner_logits) && aligned16(behavior_logits) && aligned16(d_logits);

@@ -1,6 +1,6 @@
 // Tile-resident persistent V-trace kernels (B % 4 == 0, T <= 256, A in {6, 18}).
 //
-// Same math as vtrace.cu / vtrace_tma.cu (MODE_LOGITS = from_logits, MODE_LOSS = fused
+// Same math as vtrace.cu (MODE_LOGITS = from_logits, MODE_LOSS = fused
 // learner loss; beastpipe vtrace.py:51-128 / :169-255), laid out for HBM throughput
 // at the learner's batch sizes:
 //   * a tile is BT batch columns x all T rows (BT = 4; 8 for large B); persistent CTAs
@@ -446,9 +446,8 @@ __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args 
 }  // namespace vt3
 
 // ---------------------------------------------------------------------------- host
-// BP_ERR_UNSUPPORTED when the shape is outside this kernel's regime; the caller then
-// tries the persistent kernel (vtrace_tma.cu) and finally the generic one (vtrace.cu).
-// BP_VTRACE_IMPL=2 in the environment skips this kernel (A/B measurements).
+// BP_ERR_UNSUPPORTED when the shape is outside this kernel's regime; the caller then uses
+// the generic kernel (vtrace.cu).
 int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act, const void* disc_or_done,
                const float* rew, const float* val, const float* boot, int T, int B, int A,
                float clip_rho, float clip_pg_rho, float clip_c, float discount, float pg_cost,
@@ -456,11 +455,6 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
                float* log_rhos, float* beh_logp, float* tgt_logp, float* d_logits, float* d_baseline,
                double* losses, void* workspace, size_t ws_bytes, unsigned* status, cudaStream_t s) {
   using namespace vt3;
-  static const bool disabled = [] {
-    const char* e = std::getenv("BP_VTRACE_IMPL");
-    return e && e[0] == '2';
-  }();
-  if (disabled) return BP_ERR_UNSUPPORTED;
   static const int bt_env = [] {
     const char* e = std::getenv("BP_VT3_BT");
     return e ? std::atoi(e) : 0;

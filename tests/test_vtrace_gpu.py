@@ -32,7 +32,8 @@ def _cuda(*arrs):
 
 
 SHAPES = [(20, 32, 6), (80, 32, 18), (80, 4096, 18), (7, 3, 5), (1, 1, 1), (33, 4097, 18),
-          (5, 300, 48), (80, 512, 6), (300, 20, 3), (2048, 2, 4)]
+          (5, 300, 48), (80, 512, 6), (300, 20, 3), (2048, 2, 4), (80, 514, 18), (248, 64, 6),
+          (249, 64, 18), (80, 16384, 18)]
 
 
 @pytest.mark.parametrize("T,B,A", SHAPES)

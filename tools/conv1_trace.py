@@ -10,6 +10,7 @@ from paper_1910_03552_b200 import _native as N  # noqa: E402
 from paper_1910_03552_b200.atari_net import AtariNet  # noqa: E402
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # 0 conv1, 1 conv2, 2 conv3, 3 fc, 4 heads
+keep_x0 = not (len(sys.argv) > 3 and sys.argv[3] == "nox0")
 N.lib().bp_atari_set_conv1_u8(mode)
 n = 2592
 net = AtariNet(num_actions=6)
@@ -21,7 +22,7 @@ tr = torch.zeros(148 * TT * 16, dtype=torch.int64, device="cuda")
 for it in range(3):
     if it == 2:
         N.lib().bp_gemm_trace_next(tr.data_ptr(), TT, skip)
-    net._forward_kernels(frames, rew, la, repack=True)
+    net._forward_kernels(frames, rew, la, repack=True, keep_x0=keep_x0)
 torch.cuda.synchronize()
 t = tr.view(148, TT, 16).cpu().numpy().astype(np.float64)
 ntiles = [(n * 441 + 127) // 128, (n * 100 + 127) // 128, (n * 81 + 127) // 128,
