@@ -205,9 +205,10 @@ int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const 
  * into buf[(cta * tiles + i) * 16 + event]: 0/1 producer, 2/3 MMA, 4/5 epilogue, 6/7 u8
  * converter (start / end of tile i of that CTA), 8/9 converter loop end / fence end.  buf = null cancels. */
 int bp_gemm_trace_next(void* buf, int tiles, int skip);  /* skip: traced launch = the (skip+1)-th */
-/* conv1 operand path: 1 (default) builds the conv1 A operand on chip from the u8 frames
- * (no bf16 space-to-depth grid in HBM); 0 uses the bf16 X0 grid.  Results are identical.
- * on < 0 only queries.  Returns the previous setting.  (Test / A-B knob, process-global.) */
+/* conv1 operand path: 1 (default) builds 128B-swizzled bf16 windows on chip from the u8 frames
+ * in shared memory; 2 builds im2col rows in tensor memory (the MMA reads A from TMEM);
+ * 0 uses the bf16 X0 space-to-depth grid.  Results are identical.  on < 0 only queries.
+ * Returns the previous setting.  (Test / A-B knob, process-global.) */
 int bp_atari_set_conv1_u8(int on);
 /* Conv weight-gradient path: 1 (default) = window kernel (one X window + dY box per K-block
  * feeds every m-tile of the CTA), 0 = per-tap operand boxes.  Identical sums in the same

@@ -73,14 +73,18 @@ static int make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long 
 // window mode for a shifted K-major A operand: taps share one TMA box per channel block
 // conv1 A operand straight from the u8 frames (BP_CONV1_U8=0 or bp_atari_set_conv1_u8(0) restore
 // the bf16 X0 grid path: space-to-depth kernel + TMA-loaded windows)
+// mode 1 (default): converted windows in shared memory; mode 2: im2col rows in TMEM (A operand
+// read by the MMA from tensor memory, no shared-memory A traffic, but 4x the conversion work:
+// measured 102 vs 74 us)
 static int g_conv1_u8 = -1;
-static bool conv1_u8() {
+static int conv1_u8_mode() {
   if (g_conv1_u8 < 0) {
     const char* e = std::getenv("BP_CONV1_U8");
-    g_conv1_u8 = (e && e[0] == '0') ? 0 : 1;
+    g_conv1_u8 = e ? (e[0] == '0' ? 0 : e[0] == '2' ? 2 : 1) : 1;
   }
-  return g_conv1_u8 != 0;
+  return g_conv1_u8;
 }
+static bool conv1_u8() { return conv1_u8_mode() != 0; }
 
 static void set_window(GemmArgs& g, int taps) {
   int mn = 0, mx = 0;
@@ -602,8 +606,8 @@ extern "C" int bp_atari_set_wgrad_window(int on) {
 }
 
 extern "C" int bp_atari_set_conv1_u8(int on) {
-  const int prev = conv1_u8() ? 1 : 0;
-  if (on >= 0) g_conv1_u8 = on ? 1 : 0;
+  const int prev = conv1_u8_mode();
+  if (on >= 0) g_conv1_u8 = on > 2 ? 2 : on;
   return prev;
 }
 
@@ -704,7 +708,9 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.bits_out = reinterpret_cast<uint32_t*>(net->m1);
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
-    if (conv1_u8()) {
+    if (conv1_u8_mode() == 2) {
+      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 2>(g, ta, tb, s))) return rc;
+    } else if (conv1_u8()) {
       if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 1>(g, ta, tb, s))) return rc;
     } else if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) {
       return rc;

@@ -135,13 +135,17 @@ struct GemmCfg {
   static constexpr int ACC = 2 * EPI;
   static constexpr int CONV_WARP0 = 4 + 4 * EPI;  // AU8 converter warps follow the epilogue
   static constexpr int THREADS = 128 + 128 * EPI + (AU8 ? 32 * kConvWarps : 0);
-  static constexpr uint32_t A_BYTES = AW ? kWinBytes : 128 * 64 * 2;
+  static constexpr uint32_t A_BYTES = AU8 == 2 ? 0 : AW ? kWinBytes : 128 * 64 * 2;
   static constexpr uint32_t B_BYTES = BN * 64 * 2;
-  static constexpr uint32_t STAGE = BRES ? A_BYTES : A_BYTES + B_BYTES;
+  // AU8 == 2: the A operand (im2col rows, 4 taps x 64 channels) lives in TMEM, two buffers of
+  // 128 columns after the accumulators; the "stages" are those two buffers (no smem ring)
+  static constexpr uint32_t STAGE = AU8 == 2 ? 1024 : BRES ? A_BYTES : A_BYTES + B_BYTES;
   static constexpr uint32_t B_RES = AU8 ? 16 * 1024 : BRES ? kBResBytes : 0;
   static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
-  static constexpr int STAGES = (200 * 1024 - B_RES - RAW) / STAGE > 8 ? 8 : (200 * 1024 - B_RES - RAW) / STAGE;
-  static constexpr uint32_t TMEM_COLS = (ACC * BN <= 32) ? 32 : (ACC * BN <= 64) ? 64 : (ACC * BN <= 128) ? 128 : (ACC * BN <= 256) ? 256 : 512;
+  static constexpr int STAGES = AU8 == 2 ? 2
+      : (200 * 1024 - B_RES - RAW) / STAGE > 8 ? 8 : (200 * 1024 - B_RES - RAW) / STAGE;
+  static constexpr uint32_t A_TMEM = ACC * BN;  // first TMEM column of the A buffers (AU8 == 2)
+  static constexpr uint32_t TMEM_COLS = AU8 == 2 ? 512 : (ACC * BN <= 32) ? 32 : (ACC * BN <= 64) ? 64 : (ACC * BN <= 128) ? 128 : (ACC * BN <= 256) ? 256 : 512;
   static constexpr size_t SMEM = (size_t)B_RES + RAW + (size_t)STAGES * STAGE + 1024 /*align*/ + 512 /*barriers*/ +
                                  4 * EPI * BN * sizeof(float) /*column sums*/ + 128 /*raw barriers*/;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
@@ -312,11 +316,20 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
   }
 }
 
-// two u8 (bytes k, k+1 of w) -> packed bf16x2, exact: 0x4B0000bb as f32 is 2^23 + b
+// two u8 (bytes k, k+1 of w) -> packed bf16x2, exact: 0x4B0000bb as f32 is 2^23 + b; the two
+// subtractions are one packed f32x2 add (FADD2)
 BP_DEVICE uint32_t u8pair_bf16x2(uint32_t w, int k) {
-  const float lo = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k)) - 8388608.f;
-  const float hi = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + k + 1)) - 8388608.f;
-  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632u);
+  const uint32_t m0 = __byte_perm(w, 0x4B000000u, 0x7540u + k);
+  const uint32_t m1 = __byte_perm(w, 0x4B000000u, 0x7540u + k + 1);
+  uint32_t f0, f1;
+  asm("{\n.reg .b64 a, c, d;\n"
+      "mov.b64 a, {%2, %3};\n"
+      "mov.b64 c, {%4, %4};\n"
+      "add.rn.f32x2 d, a, c;\n"
+      "mov.b64 {%0, %1}, d;\n}\n"
+      : "=r"(f0), "=r"(f1)
+      : "r"(m0), "r"(m1), "r"(0xCB000000u));  // -2^23
+  return __byte_perm(f0, f1, 0x7632u);
 }
 
 // u8 plane of (img, ci) (AU8 frame source)
@@ -418,6 +431,76 @@ BP_DEVICE void u8_stage_convert(const Args& g, long long r0, int nrows, const ui
         __stcs(reinterpret_cast<uint4*>(g.u8_x0_out + (r0 + rr) * 64) + j, v);
     }
   }
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16: A (M = 128 rows = TMEM lanes, K along columns,
+// two bf16 per 32-bit column) read from tensor memory
+BP_DEVICE void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit: thread i of the warp writes lane (base + i)
+BP_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+BP_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// AU8 == 2 converter warp (quadrant q = TMEM lanes [32q, 32q + 32), half h = taps 2h, 2h + 1):
+// the im2col row of tile row rr = 32q + lane for those taps -- 64 channels of window row
+// rr + off_tap each -- converted from the raw stage and stored to the TMEM A buffer at
+// column a_col + 32 tap.  Tap 0 is the tile's own row: it also goes to HBM as X0 (optional).
+template <class Args>
+BP_DEVICE void u8_im2col_tmem(const Args& g, long long r0, const uint8_t* raw, uint32_t tmem_a, int q, int h,
+                              int lane) {
+  const uint32_t r0u = (uint32_t)r0;
+  const int x0 = (int)(r0u - fdivu(r0u, FDiv{0x86186187u, 5u}) * 21u);  // r0 % 21 (r0 < 2^31)
+  const long long left = g.u8_rows - r0;
+  const int rr = q * 32 + lane;
+  const uint32_t sraw = after_wait(sm100::smem_addr(raw));
+#pragma unroll
+  for (int tt = 0; tt < 2; ++tt) {
+    const int t = 2 * h + tt;
+    const int wr = rr + g.a_row_off[t];
+    uint32_t v[32];
+    if (wr < left) {
+      const int qq = x0 + wr;
+      const int gs = qq / 21;
+      const uint32_t base = sraw + gs * kRawRowBytes + 4 * (qq - gs * 21);
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) w[k] = lds_u32(base + (k >> 2) * kRawCiBytes + (k & 3) * 84);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        v[2 * k] = u8pair_bf16x2(w[k], 0);
+        v[2 * k + 1] = u8pair_bf16x2(w[k], 2);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = 0u;
+    }
+    tmem_st_32x32b_x32(tmem_a + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * 32), v);
+    if (t == 0 && g.u8_x0_out && rr < left) {
+      uint4* o = reinterpret_cast<uint4*>(g.u8_x0_out + (r0 + rr) * 64);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) __stcs(o + k, make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+    }
+  }
+  tmem_st_wait();
 }
 
 template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
@@ -545,7 +628,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       sm100::tc_fence_after();
       if (lane == 0) trace_ev(g, ti, 2);
       const uint32_t d = tmem_base + acc * BN;
-      if constexpr (AW > 0) {
+      if constexpr (AU8 == 2) {  // A = the im2col buffer in TMEM, B = the resident weights
+        sm100::mbar_wait(&full[stage], phase);
+        sm100::tc_fence_after();
+        const uint32_t ta = tmem_base + C::A_TMEM + (uint32_t)stage * 128u;
+        if (sm100::elect_one()) {
+          for (int t = 0; t < g.a_ntaps; ++t) {
+            const uint32_t sb = sm100::smem_addr(bres + t * C::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_f16_ts(d, ta + (uint32_t)(t * 32 + k * 8), b_hi | ((sb + k * b_kstep) >> 4), idesc,
+                          (t > 0 || k > 0) ? 1u : 0u);
+          }
+          sm100::umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      } else if constexpr (AW > 0) {
         for (int cb = 0; cb < g.a_cb; ++cb) {
           sm100::mbar_wait(&full[stage], phase);
           sm100::tc_fence_after();
@@ -598,11 +697,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       sm100::mbar_wait(&raw_full[rs], rph);
       sm100::mbar_wait(&empty[stage], phase ^ 1);
       if (c == 0) trace_ev(g, ti, 6);
-      u8_stage_convert(g, (long long)mt * 128 + g.a_min_off, g.a_win_rows, rawr + rs * kRawBytes,
-                       ring + stage * C::STAGE, c, 128 - g.a_min_off);
+      if constexpr (AU8 == 2) {
+        sm100::tc_fence_after();
+        const int cw = warp - C::CONV_WARP0;
+        u8_im2col_tmem(g, (long long)mt * 128, rawr + rs * kRawBytes,
+                       tmem_base + C::A_TMEM + (uint32_t)stage * 128u, warp & 3, cw >> 2, threadIdx.x & 31);
+        sm100::tc_fence_before();  // tcgen05.st -> the MMA warp's reads, ordered by the barrier
+      } else {
+        u8_stage_convert(g, (long long)mt * 128 + g.a_min_off, g.a_win_rows, rawr + rs * kRawBytes,
+                         ring + stage * C::STAGE, c, 128 - g.a_min_off);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> UMMA reads
+      }
       if (c == 0) trace_ev(g, ti, 8);
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> UMMA reads
-      if (c == 0) trace_ev(g, ti, 9);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) {
         sm100::mbar_arrive(&full[stage]);

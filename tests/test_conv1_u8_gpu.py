@@ -18,8 +18,9 @@ def _run(net, frames, reward, la, mode, **kw):
         N.lib().bp_atari_set_conv1_u8(prev)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("n", [1, 7, 64, 300])
-def test_conv1_u8_forward_bit_identical(n):
+def test_conv1_u8_forward_bit_identical(n, mode):
     from paper_1910_03552_b200.atari_net import AtariNet
 
     torch.manual_seed(n)
@@ -28,11 +29,12 @@ def test_conv1_u8_forward_bit_identical(n):
     reward = torch.rand(n, device="cuda")
     la = torch.randint(0, 6, (n,), device="cuda")
     a = _run(net, frames, reward, la, 0)
-    b = _run(net, frames, reward, la, 1)
+    b = _run(net, frames, reward, la, mode)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
 
 
-def test_conv1_u8_plane_store_bit_identical():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_conv1_u8_plane_store_bit_identical(mode):
     from paper_1910_03552_b200 import rollout
     from paper_1910_03552_b200.atari_net import AtariNet
 
@@ -47,11 +49,12 @@ def test_conv1_u8_plane_store_bit_identical():
     reward = torch.rand(n, device="cuda")
     la = torch.randint(0, 6, (n,), device="cuda")
     a = _run(net, frames, reward, la, 0)
-    b = _run(net, planes, reward, la, 1, plane_index=idx.reshape(n, 4))
+    b = _run(net, planes, reward, la, mode, plane_index=idx.reshape(n, 4))
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
 
 
-def test_conv1_u8_backward_bit_identical():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_conv1_u8_backward_bit_identical(mode):
     """The converter's X0 side output feeds the conv1 weight gradient: whole-network
     gradients must equal the space-to-depth path bit for bit."""
     from paper_1910_03552_b200.atari_net import AtariNet
@@ -65,8 +68,8 @@ def test_conv1_u8_backward_bit_identical():
     dl = torch.randn(n, 6, device="cuda")
     db = torch.randn(n, device="cuda")
     grads = []
-    for mode in (0, 1):
-        prev = N.lib().bp_atari_set_conv1_u8(mode)
+    for m in (0, mode):
+        prev = N.lib().bp_atari_set_conv1_u8(m)
         try:
             net._forward_kernels(frames, reward, la, repack=True)
             g = torch.empty_like(net.flat_params)
