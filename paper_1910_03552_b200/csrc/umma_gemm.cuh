@@ -143,11 +143,12 @@ struct GemmCfg {
   static constexpr uint32_t B_RES = AU8 ? 16 * 1024 : BRES ? kBResBytes : 0;
   static constexpr uint32_t RAW = AU8 ? kRawStages * kRawBytes : 0;
   static constexpr int STAGES = AU8 == 2 ? 2
-      : (200 * 1024 - B_RES - RAW) / STAGE > 8 ? 8 : (200 * 1024 - B_RES - RAW) / STAGE;
+      : (184 * 1024 - B_RES - RAW) / STAGE > 8 ? 8 : (184 * 1024 - B_RES - RAW) / STAGE;
   static constexpr uint32_t A_TMEM = ACC * BN;  // first TMEM column of the A buffers (AU8 == 2)
   static constexpr uint32_t TMEM_COLS = AU8 == 2 ? 512 : (ACC * BN <= 32) ? 32 : (ACC * BN <= 64) ? 64 : (ACC * BN <= 128) ? 128 : (ACC * BN <= 256) ? 256 : 512;
+  static constexpr uint32_t OSTAGE = 4 * EPI * 2048;  // per epilogue warp: 32 rows x 64 B bf16 staging
   static constexpr size_t SMEM = (size_t)B_RES + RAW + (size_t)STAGES * STAGE + 1024 /*align*/ + 512 /*barriers*/ +
-                                 4 * EPI * BN * sizeof(float) /*column sums*/ + 128 /*raw barriers*/;
+                                 4 * EPI * BN * sizeof(float) /*column sums*/ + 256 /*raw barriers + align*/ + OSTAGE;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(BM == B_KMAJOR || BSWZ == 128 || (BSWZ == 64 && BN == 32), "B swizzle");
 };
@@ -241,7 +242,7 @@ BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 // csum_acc: per-CTA running column sum for this lane's column (null: per-tile partial rows)
 BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
                               int sp, int mt, int ew, int lane, float (&v)[32], uint32_t mkw,
-                              float* csum_acc) {
+                              float* csum_acc, uint32_t ostage) {
   if (n0 >= g.N) return;  // a partial last column tile (warp-uniform)
   if (g.heads) {
     if (row_ok) {
@@ -278,11 +279,12 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
     for (int i = 0; i < 32; ++i)
       if (!((w >> i) & 1u)) v[i] = 0.f;
   }
+  long long off = -1;  // element offset of this lane's row chunk (-1: row not stored)
   if (row_ok) {
     const uint32_t qd = fdivu((uint32_t)n0, g.fd_cdiv), q1 = fdivu(qd, g.fd_cq);
     const long long cbase = (long long)q1 * g.cs1 + (long long)(qd - q1 * (uint32_t)g.cq) * g.cs2 +
                             (long long)((uint32_t)n0 - qd * (uint32_t)g.cdiv);
-    const long long off = rbase + cbase + (long long)sp * g.split_stride;
+    off = rbase + cbase + (long long)sp * g.split_stride;
     if (g.bits_out) {
       uint32_t bits = 0;
 #pragma unroll
@@ -297,13 +299,38 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
       float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else {
+    } else if (!ostage) {
       uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out) + off);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
     }
+  }
+  if (!g.out_f32 && ostage) {
+    // bf16 rows through a per-warp 2 KB staging buffer: every lane writes its 64-byte row chunk
+    // (16-byte pieces XOR-swizzled by row pair: conflict-free), then each store instruction
+    // writes 8 rows x 64 contiguous bytes (4 lanes per row) instead of 32 scattered 16-byte
+    // pieces -- full sectors and 4x fewer L1 -> L2 write transactions
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(ostage + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)),
+                   "r"(pack_bf16x2(v[8 * q], v[8 * q + 1])), "r"(pack_bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                   "r"(pack_bf16x2(v[8 * q + 4], v[8 * q + 5])), "r"(pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                   : "memory");
+    __syncwarp();
+    char* outb = reinterpret_cast<char*>(g.out);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int p = k * 32 + lane, row = p >> 2, sub = p & 3;
+      const long long ro = __shfl_sync(0xffffffffu, off, row);
+      uint32_t a, b, c, d;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                   : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                   : "r"(ostage + row * 64 + ((sub ^ ((row >> 1) & 3)) << 4)));
+      if (ro >= 0) *reinterpret_cast<uint4*>(outb + ro * 2 + sub * 16) = make_uint4(a, b, c, d);
+    }
+    __syncwarp();  // the buffer is reused by the next chunk
   }
   if (g.colsum) {  // warp-uniform branch
     if (!row_ok) {
@@ -524,6 +551,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
   float* csum_smem = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bfull) + 64);  // [4 * EPI][BN]
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(csum_smem + 4 * C::EPI * BN);        // AU8
   uint64_t* raw_empty = raw_full + kRawStages;
+  uint8_t* ostage_base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_empty + kRawStages) + 127) &
+                                                    ~uintptr_t(127));  // [4 * EPI][2048] bf16 staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -723,6 +752,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
     // warp ew of a group reads TMEM lanes [32 ew, 32 ew + 32)
     const int grp = (warp - 4) >> 2, ew = (warp - 4) & 3;
     constexpr int NCH = BN / 32;
+    const uint32_t ostage = sm100::smem_addr(ostage_base + (warp - 4) * 2048);
     // bias-gradient column sums: accumulated per CTA (per epilogue warp, in shared memory)
     // when every tile covers the same columns; otherwise written per tile
     const bool cta_colsum = g.colsum && g.n_tiles == 1 && g.splits == 1;
@@ -730,53 +760,88 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
     if (cta_colsum) {
       for (int c = 0; c < NCH; ++c) csum[c * 32 + lane] = 0.f;
     }
-    for (int ti = grp, tile = blockIdx.x + grp * gridDim.x; tile < ntiles;
-         ti += C::EPI, tile += C::EPI * gridDim.x) {
-      const int acc = ti % C::ACC;
-      const uint32_t aphase = (uint32_t)(ti / C::ACC) & 1u;
-      int mt, nt, sp;
-      tile_coords(g, tile, mt, nt, sp);
-      const int m = mt * 128 + ew * 32 + lane;
-      // row map
-      bool row_ok = m < g.M;
-      long long rbase = 0;
+    // row map + relu-mask words of a tile (the masks are prefetched one tile ahead: when the
+    // epilogue is the bottleneck the accumulator is already waiting, so loads issued just
+    // before the tfull wait would not be hidden)
+    struct RowInfo {
+      int m, mt, nt, sp;
+      bool ok;
+      long long rbase;
+      uint32_t mk[4];
+    };
+    auto row_info = [&](int tile) {
+      RowInfo ri;
+      tile_coords(g, tile, ri.mt, ri.nt, ri.sp);
+      ri.m = ri.mt * 128 + ew * 32 + lane;
+      ri.ok = ri.m < g.M;
       {  // precomputed-multiplier divisions (m < 2^31)
-        const uint32_t mu = (uint32_t)m;
+        const uint32_t mu = (uint32_t)ri.m;
         const uint32_t img = fdivu(mu, g.fd_per);
         const uint32_t rem = mu - img * (uint32_t)(g.gh * g.gw);
         const uint32_t y = fdivu(rem, g.fd_gw);
         const uint32_t x = rem - y * (uint32_t)g.gw;
         const uint32_t ys = fdivu(y, g.fd_sy), xs = fdivu(x, g.fd_sx);
-        row_ok = row_ok && ((int)y < g.vh) && ((int)x < g.vw);
-        rbase = (long long)img * g.r_img + (long long)ys * g.r_y + (long long)xs * g.r_x +
-                (long long)((y - ys * (uint32_t)g.sy) * (uint32_t)g.sx + (x - xs * (uint32_t)g.sx)) * g.r_sub;
+        ri.ok = ri.ok && ((int)y < g.vh) && ((int)x < g.vw);
+        ri.rbase = (long long)img * g.r_img + (long long)ys * g.r_y + (long long)xs * g.r_x +
+                   (long long)((y - ys * (uint32_t)g.sy) * (uint32_t)g.sx + (x - xs * (uint32_t)g.sx)) * g.r_sub;
       }
-      // prefetch the tile's relu-mask words (one u32 per 32 columns) before waiting for the
-      // accumulator, so their latency overlaps the MMAs (masked GEMMs have BN <= 128)
-      uint32_t mk0 = 0, mk1 = 0, mk2 = 0, mk3 = 0;
-      if (g.mask_bits && row_ok) {
-        const uint32_t* mp = g.mask_bits + (((size_t)m * (g.mask_ld ? g.mask_ld : g.N) + nt * BN) >> 5);
-        const int nc = nt * BN;  // only the chunks inside N (a partial last column tile)
-        mk0 = __ldg(mp);
-        if (NCH > 1 && nc + 32 < g.N) mk1 = __ldg(mp + 1);
-        if (NCH > 2 && nc + 64 < g.N) mk2 = __ldg(mp + 2);
-        if (NCH > 3 && nc + 96 < g.N) mk3 = __ldg(mp + 3);
+      ri.mk[0] = ri.mk[1] = ri.mk[2] = ri.mk[3] = 0u;
+      if (g.mask_bits && ri.ok) {
+        const uint32_t* mp = g.mask_bits + (((size_t)ri.m * (g.mask_ld ? g.mask_ld : g.N) + ri.nt * BN) >> 5);
+        const int nc = ri.nt * BN;  // only the chunks inside N (a partial last column tile)
+        ri.mk[0] = __ldg(mp);
+        if (NCH > 1 && nc + 32 < g.N) ri.mk[1] = __ldg(mp + 1);
+        if (NCH > 2 && nc + 64 < g.N) ri.mk[2] = __ldg(mp + 2);
+        if (NCH > 3 && nc + 96 < g.N) ri.mk[3] = __ldg(mp + 3);
       }
+      return ri;
+    };
+    const int tile_step = C::EPI * gridDim.x;
+    RowInfo nxt{};
+    if ((int)blockIdx.x + grp * (int)gridDim.x < ntiles) nxt = row_info(blockIdx.x + grp * gridDim.x);
+    for (int ti = grp, tile = blockIdx.x + grp * gridDim.x; tile < ntiles; ti += C::EPI, tile += tile_step) {
+      const int acc = ti % C::ACC;
+      const uint32_t aphase = (uint32_t)(ti / C::ACC) & 1u;
+      const RowInfo cur = nxt;
+      if (tile + tile_step < ntiles) nxt = row_info(tile + tile_step);
+      const int m = cur.m, mt = cur.mt, nt = cur.nt, sp = cur.sp;
+      const bool row_ok = cur.ok;
+      const long long rbase = cur.rbase;
+      const uint32_t mk0 = cur.mk[0], mk1 = cur.mk[1], mk2 = cur.mk[2], mk3 = cur.mk[3];
       sm100::mbar_wait(&tfull[acc], aphase);
       sm100::tc_fence_after();
       if (ew == 0 && lane == 0) trace_ev(g, ti, 4);
       const bool has_k = (sp * g.kb_per_split) < g.num_kb;
-#pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
-        sm100::tmem_ld_wait();
-        float v[32];
+      // TMEM loads one chunk ahead: the load of chunk c + 1 is in flight while chunk c is
+      // processed (tcgen05.wait::ld waits for all earlier loads, so it is issued right after)
+      // (BN <= 64; for 4 chunks the extra 32 live registers cost more than the overlap gains)
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(ew * 32) << 16);
+      if constexpr (NCH <= 2) {
+        uint32_t rbuf[2][32];
+        sm100::tmem_ld_32x32b_x32(tbase, rbuf[0]);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(r[i]) : 0.f;
-        const uint32_t mkw = c == 0 ? mk0 : c == 1 ? mk1 : c == 2 ? mk2 : mk3;
-        epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, mkw,
-                       cta_colsum ? &csum[c * 32 + lane] : nullptr);
+        for (int c = 0; c < NCH; ++c) {
+          sm100::tmem_ld_wait();
+          if (c + 1 < NCH) sm100::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rbuf[(c + 1) & 1]);
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(rbuf[c & 1][i]) : 0.f;
+          epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, c == 0 ? mk0 : mk1,
+                         cta_colsum ? &csum[c * 32 + lane] : nullptr, ostage);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t r[32];
+          sm100::tmem_ld_32x32b_x32(tbase + c * 32, r);
+          sm100::tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(r[i]) : 0.f;
+          const uint32_t mkw = c == 0 ? mk0 : c == 1 ? mk1 : c == 2 ? mk2 : mk3;
+          epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, mkw,
+                         cta_colsum ? &csum[c * 32 + lane] : nullptr, ostage);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
