@@ -147,7 +147,7 @@ static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUten
   kern<<<g.splits, Cfg::THREADS, Cfg::SMEM, s>>>(g, tx, ty);
   return check_launch("umma_wgrad_win_kernel");
 }
-template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0, int EK = EPK_GEN>
 static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensorMap& tb, cudaStream_t s) {
   GemmArgs g = g0;
   gemm_prepare(g);
@@ -163,7 +163,15 @@ static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensor
     }
   }
   using Cfg = GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>;
-  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW, AU8>;
+  auto kern = umma_gemm_kernel<BN, AM, BM, BSWZ, BRES, AW, AU8, EK>;
+  if (EK == EPK_FWD && (!g.bias || !g.relu || g.out_f32 || g.heads || g.mask_bits || g.colsum)) {
+    set_error("gemm: forward epilogue needs bias + relu, bf16 out");
+    return 1;
+  }
+  if (EK == EPK_DGRAD && (!g.mask_bits || g.out_f32 || g.heads || g.bias || g.relu || g.bits_out)) {
+    set_error("gemm: data-gradient epilogue needs a mask, bf16 out");
+    return 1;
+  }
   if (AW && (g.a_win_rows > 160 || g.a_win_rows < 128 || g.a_ntaps < 1 || g.a_ntaps > kMaxShifts)) {
     set_error("gemm: window rows %d / taps %d unsupported", g.a_win_rows, g.a_ntaps);
     return BP_ERR_ARG;
@@ -709,10 +717,10 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
     if (conv1_u8_mode() == 2) {
-      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 2>(g, ta, tb, s))) return rc;
+      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 2, EPK_FWD>(g, ta, tb, s))) return rc;
     } else if (conv1_u8()) {
-      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 1>(g, ta, tb, s))) return rc;
-    } else if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) {
+      if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 1, EPK_FWD>(g, ta, tb, s))) return rc;
+    } else if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 0, EPK_FWD>(g, ta, tb, s))) {
       return rc;
     }
   }
@@ -737,7 +745,7 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.bits_out = reinterpret_cast<uint32_t*>(net->m2);
     g.gh = 10; g.gw = 10; g.vh = 9; g.vw = 9;
     g.r_img = 81 * 64; g.r_y = 9 * 64; g.r_x = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1, 0, EPK_FWD>(g, ta, tb, s))) return rc;
   }
   // 4. conv3: X2 [n*81, 64], 3x3 taps on the 9x9 grid -> X3 [n, 3136] ((y, x, c) order)
   {
@@ -759,7 +767,7 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.bits_out = reinterpret_cast<uint32_t*>(net->m3);
     g.gh = 9; g.gw = 9; g.vh = 7; g.vw = 7;
     g.r_img = 3136; g.r_y = 7 * 64; g.r_x = 64;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1, 0, EPK_FWD>(g, ta, tb, s))) return rc;
   }
   // 5. fc: X3 [n, 3136] x Wfc [512, 3136] -> core[:, :512] = relu(. + bfc)
   {
@@ -781,8 +789,8 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.out = net->core;
     g.bits_out = reinterpret_cast<uint32_t*>(net->mc);
     g.r_img = kCoreW;
-    if ((rc = wide ? launch_gemm<128, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s)
-                   : launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s)))
+    if ((rc = wide ? launch_gemm<128, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_FWD>(g, ta, tb, s)
+                   : launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_FWD>(g, ta, tb, s)))
       return rc;
   }
   return BP_OK;
@@ -921,8 +929,8 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[2];  // window mode: bias from the wgrad ones atom
     if (wgrad_window()) {  // 128-column tiles (the last half empty): d_fc re-read 25x instead of 49x
       g.n_tiles = 25;
-      if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
-    } else if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) {
+      if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_DGRAD>(g, ta, tb, s))) return rc;
+    } else if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_DGRAD>(g, ta, tb, s))) {
       return rc;
     }
   }
@@ -947,7 +955,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.gh = 9; g.gw = 9; g.vh = 9; g.vw = 9;
     g.r_img = 100 * 64; g.r_y = 10 * 64; g.r_x = 64;
     g.colsum = ws + P.cs_off[1];  // db2
-    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1, 0, EPK_DGRAD>(g, ta, tb, s))) return rc;
   }
   // conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
   {
@@ -971,7 +979,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.r_img = 441 * 32; g.r_y = 2 * 21 * 32; g.r_x = 2 * 32;
     g.cdiv = 32; g.cq = 2; g.cs1 = 21 * 32; g.cs2 = 32;
     g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[0];  // window mode: bias from the wgrad ones atom
-    if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1, 0, EPK_DGRAD>(g, ta, tb, s))) return rc;
   }
   // weight gradients
   auto wgrad = [&](int i, const void* X, long long xrows, int xcols, int atoms_per_shift, int nshifts,

@@ -128,11 +128,17 @@ constexpr uint32_t kRawBytes = 12288;                       // >= 4 * 3024, 1 KB
 constexpr int kRawStages = 4;
 constexpr int kConvWarps = 8;  // AU8 converter warps (after the epilogue warps)
 
+#ifndef BP_EPI_GROUPS
+#define BP_EPI_GROUPS 3
+#endif
+constexpr int kEpiGroups = BP_EPI_GROUPS;
+
 template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
 struct GemmCfg {
-  // two epilogue warpgroups take alternate tiles (4 TMEM accumulators) when 4 * BN fits
-  static constexpr int EPI = (4 * BN <= 512) ? 2 : 1;
-  static constexpr int ACC = 2 * EPI;
+  // EPI epilogue warpgroups take the CTA's tiles in turn (the epilogue is the per-tile
+  // bottleneck of these small-N GEMMs); one or two TMEM accumulators per group
+  static constexpr int EPI = BN > 128 ? 1 : AU8 ? 2 : kEpiGroups;
+  static constexpr int ACC = 2 * EPI * BN <= 512 ? 2 * EPI : EPI;
   static constexpr int CONV_WARP0 = 4 + 4 * EPI;  // AU8 converter warps follow the epilogue
   static constexpr int THREADS = 128 + 128 * EPI + (AU8 ? 32 * kConvWarps : 0);
   static constexpr uint32_t A_BYTES = AU8 == 2 ? 0 : AW ? kWinBytes : 128 * 64 * 2;
@@ -222,6 +228,12 @@ BP_DEVICE uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+BP_DEVICE uint32_t ldg_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // lane j ends with sum over the warp's 32 lanes of v[j] (31 shuffles, fixed order)
 BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 #pragma unroll
@@ -237,14 +249,31 @@ BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
   return v[0];
 }
 
+// Epilogue kinds (compile time; the hot GEMMs drop the runtime feature checks):
+//   EPK_GEN   every feature from GemmArgs at run time (f32 partials, heads, tests);
+//   EPK_FWD   conv / fc forward: alpha * acc + bias, ReLU, relu bits (when bits_out), bf16 out;
+//   EPK_DGRAD data gradient: relu-backward mask, bf16 out, optional column sums.
+enum { EPK_GEN = 0, EPK_FWD = 1, EPK_DGRAD = 2 };
+
+// element offset of column n (the column map; n is warp-uniform)
+BP_DEVICE long long col_offset(const GemmArgs& g, int n) {
+  const uint32_t qd = fdivu((uint32_t)n, g.fd_cdiv), q1 = fdivu(qd, g.fd_cq);
+  return (long long)q1 * g.cs1 + (long long)(qd - q1 * (uint32_t)g.cq) * g.cs2 + (long long)((uint32_t)n - qd * (uint32_t)g.cdiv);
+}
+
 // one row x 32 consecutive columns of the tile (called by all 32 lanes of an epilogue warp)
-// mkw: the prefetched relu-mask word of this row chunk (when g.mask_bits);
-// csum_acc: per-CTA running column sum for this lane's column (null: per-tile partial rows)
-BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, int m, int n0,
-                              int sp, int mt, int ew, int lane, float (&v)[32], uint32_t mkw,
-                              float* csum_acc, uint32_t ostage) {
+// roff: this lane's row offset (row map + split; -1: row not stored); sro[k]: roff of row
+// 8k + lane/4 (the rows this lane writes in the staged store); mkw: the prefetched relu-mask
+// word of this row chunk (when g.mask_bits); csum_acc: per-CTA running column sum for this
+// lane's column (null: per-tile partial rows)
+template <int EK>
+BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long (&sro)[4], int m, int n0,
+                              int mt, int ew, int lane, float (&v)[32], uint32_t mkw, float* csum_acc,
+                              uint32_t ostage) {
   if (n0 >= g.N) return;  // a partial last column tile (warp-uniform)
-  if (g.heads) {
+  const bool row_ok = roff >= 0;
+  constexpr bool GEN = EK == EPK_GEN;
+  if (GEN && g.heads) {
     if (row_ok) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {  // compile-time indices keep v[] in registers
@@ -254,7 +283,7 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
     }
     return;
   }
-  if (g.bias) {  // alpha * acc + bias; the 32 bias values as 8 broadcast 16-byte loads
+  if (EK == EPK_FWD || (GEN && g.bias)) {  // alpha * acc + bias; the 32 bias values as 8 broadcast 16-byte loads
     const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0);
     const float al = g.alpha;
 #pragma unroll
@@ -265,49 +294,39 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
       v[4 * q + 2] = fmaf(v[4 * q + 2], al, b.z);
       v[4 * q + 3] = fmaf(v[4 * q + 3], al, b.w);
     }
-  } else if (g.alpha != 1.f) {
+  } else if (GEN && g.alpha != 1.f) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= g.alpha;
   }
-  if (g.relu) {
+  if (EK == EPK_FWD || (GEN && g.relu)) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
   }
-  if (g.mask_bits && row_ok) {
-    const uint32_t w = mkw;
+  if (EK == EPK_DGRAD || (GEN && g.mask_bits)) {  // (mkw is 0 for rows outside the grid)
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (!((w >> i) & 1u)) v[i] = 0.f;
+      if (!((mkw >> i) & 1u)) v[i] = 0.f;
   }
-  long long off = -1;  // element offset of this lane's row chunk (-1: row not stored)
+  const long long coff = col_offset(g, n0);
   if (row_ok) {
-    const uint32_t qd = fdivu((uint32_t)n0, g.fd_cdiv), q1 = fdivu(qd, g.fd_cq);
-    const long long cbase = (long long)q1 * g.cs1 + (long long)(qd - q1 * (uint32_t)g.cq) * g.cs2 +
-                            (long long)((uint32_t)n0 - qd * (uint32_t)g.cdiv);
-    off = rbase + cbase + (long long)sp * g.split_stride;
-    if (g.bits_out) {
+    const long long off = roff + coff;
+    if (EK != EPK_DGRAD && g.bits_out) {
       uint32_t bits = 0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) bits |= (v[i] > 0.f ? 1u : 0u) << i;
       g.bits_out[off >> 5] = bits;
     }
-    if (g.out_f32 && g.col_stride) {  // transposed store: per column, the warp's 32 rows are contiguous
+    if (GEN && g.out_f32 && g.col_stride) {  // transposed store: per column, the warp's 32 rows are contiguous
       float* o = reinterpret_cast<float*>(g.out) + off;
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[(long long)i * g.col_stride] = v[i];
-    } else if (g.out_f32) {
+    } else if (GEN && g.out_f32) {
       float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else if (!ostage) {
-      uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out) + off);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                          pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
     }
   }
-  if (!g.out_f32 && ostage) {
+  if (!GEN || !g.out_f32) {
     // bf16 rows through a per-warp 2 KB staging buffer: every lane writes its 64-byte row chunk
     // (16-byte pieces XOR-swizzled by row pair: conflict-free), then each store instruction
     // writes 8 rows x 64 contiguous bytes (4 lanes per row) instead of 32 scattered 16-byte
@@ -319,20 +338,20 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long rbase, bool row_ok, i
                    "r"(pack_bf16x2(v[8 * q + 4], v[8 * q + 5])), "r"(pack_bf16x2(v[8 * q + 6], v[8 * q + 7]))
                    : "memory");
     __syncwarp();
-    char* outb = reinterpret_cast<char*>(g.out);
+    char* outb = reinterpret_cast<char*>(g.out) + coff * 2;
+    const int sub = lane & 3;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int p = k * 32 + lane, row = p >> 2, sub = p & 3;
-      const long long ro = __shfl_sync(0xffffffffu, off, row);
+      const int row = k * 8 + (lane >> 2);
       uint32_t a, b, c, d;
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                    : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
                    : "r"(ostage + row * 64 + ((sub ^ ((row >> 1) & 3)) << 4)));
-      if (ro >= 0) *reinterpret_cast<uint4*>(outb + ro * 2 + sub * 16) = make_uint4(a, b, c, d);
+      if (sro[k] >= 0) *reinterpret_cast<uint4*>(outb + sro[k] * 2 + sub * 16) = make_uint4(a, b, c, d);
     }
     __syncwarp();  // the buffer is reused by the next chunk
   }
-  if (g.colsum) {  // warp-uniform branch
+  if (EK != EPK_FWD && g.colsum) {  // warp-uniform branch
     if (!row_ok) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -530,7 +549,7 @@ BP_DEVICE void u8_im2col_tmem(const Args& g, long long r0, const uint8_t* raw, u
   tmem_st_wait();
 }
 
-template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0>
+template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0, int EK = EPK_GEN>
 __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB) {
@@ -755,7 +774,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
     const uint32_t ostage = sm100::smem_addr(ostage_base + (warp - 4) * 2048);
     // bias-gradient column sums: accumulated per CTA (per epilogue warp, in shared memory)
     // when every tile covers the same columns; otherwise written per tile
-    const bool cta_colsum = g.colsum && g.n_tiles == 1 && g.splits == 1;
+    const bool cta_colsum = EK != EPK_FWD && g.colsum && g.n_tiles == 1 && g.splits == 1;
     float* csum = csum_smem + (grp * 4 + ew) * BN;
     if (cta_colsum) {
       for (int c = 0; c < NCH; ++c) csum[c * 32 + lane] = 0.f;
@@ -786,13 +805,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
                    (long long)((y - ys * (uint32_t)g.sy) * (uint32_t)g.sx + (x - xs * (uint32_t)g.sx)) * g.r_sub;
       }
       ri.mk[0] = ri.mk[1] = ri.mk[2] = ri.mk[3] = 0u;
-      if (g.mask_bits && ri.ok) {
+      if ((EK == EPK_DGRAD || (EK == EPK_GEN && g.mask_bits)) && ri.ok) {
         const uint32_t* mp = g.mask_bits + (((size_t)ri.m * (g.mask_ld ? g.mask_ld : g.N) + ri.nt * BN) >> 5);
         const int nc = ri.nt * BN;  // only the chunks inside N (a partial last column tile)
-        ri.mk[0] = __ldg(mp);
-        if (NCH > 1 && nc + 32 < g.N) ri.mk[1] = __ldg(mp + 1);
-        if (NCH > 2 && nc + 64 < g.N) ri.mk[2] = __ldg(mp + 2);
-        if (NCH > 3 && nc + 96 < g.N) ri.mk[3] = __ldg(mp + 3);
+        // volatile: issued here, a tile ahead of use (a plain __ldg may be sunk to its use)
+        ri.mk[0] = ldg_volatile(mp);
+        if (NCH > 1 && nc + 32 < g.N) ri.mk[1] = ldg_volatile(mp + 1);
+        if (NCH > 2 && nc + 64 < g.N) ri.mk[2] = ldg_volatile(mp + 2);
+        if (NCH > 3 && nc + 96 < g.N) ri.mk[3] = ldg_volatile(mp + 3);
       }
       return ri;
     };
@@ -805,18 +825,28 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       const RowInfo cur = nxt;
       if (tile + tile_step < ntiles) nxt = row_info(tile + tile_step);
       const int m = cur.m, mt = cur.mt, nt = cur.nt, sp = cur.sp;
-      const bool row_ok = cur.ok;
-      const long long rbase = cur.rbase;
       const uint32_t mk0 = cur.mk[0], mk1 = cur.mk[1], mk2 = cur.mk[2], mk3 = cur.mk[3];
+      // this lane's row offset (-1: not stored) and those of the rows it writes in the staged
+      // bf16 store (row 8k + lane/4), once per tile
+      const long long roff = cur.ok ? cur.rbase + (long long)sp * g.split_stride : -1ll;
+      long long sro[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sro[k] = __shfl_sync(0xffffffffu, roff, k * 8 + (lane >> 2));
       sm100::mbar_wait(&tfull[acc], aphase);
       sm100::tc_fence_after();
       if (ew == 0 && lane == 0) trace_ev(g, ti, 4);
-      const bool has_k = (sp * g.kb_per_split) < g.num_kb;
-      // TMEM loads one chunk ahead: the load of chunk c + 1 is in flight while chunk c is
-      // processed (tcgen05.wait::ld waits for all earlier loads, so it is issued right after)
-      // (BN <= 64; for 4 chunks the extra 32 live registers cost more than the overlap gains)
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(ew * 32) << 16);
-      if constexpr (NCH <= 2) {
+      if ((sp * g.kb_per_split) >= g.num_kb) {  // an empty split-K range: no MMA wrote the accumulator
+        uint32_t z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0u;
+        for (int c = 0; c < NCH; ++c) tmem_st_32x32b_x32(tbase + c * 32, z);
+        tmem_st_wait();
+      }
+      if constexpr (NCH <= 2 && C::EPI <= 2) {
+        // TMEM loads one chunk ahead: the load of chunk c + 1 is in flight while chunk c is
+        // processed (tcgen05.wait::ld waits for all earlier loads, so it is issued right after).
+        // (BN <= 64; for 4 chunks the extra 32 live registers cost more than the overlap gains)
         uint32_t rbuf[2][32];
         sm100::tmem_ld_32x32b_x32(tbase, rbuf[0]);
 #pragma unroll
@@ -825,8 +855,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
           if (c + 1 < NCH) sm100::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rbuf[(c + 1) & 1]);
           float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(rbuf[c & 1][i]) : 0.f;
-          epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, c == 0 ? mk0 : mk1,
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rbuf[c & 1][i]);
+          epilogue_chunk<EK>(g, roff, sro, m, nt * BN + c * 32, mt, ew, lane, v, c == 0 ? mk0 : mk1,
                          cta_colsum ? &csum[c * 32 + lane] : nullptr, ostage);
         }
       } else {
@@ -837,9 +867,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
           sm100::tmem_ld_wait();
           float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = has_k ? __uint_as_float(r[i]) : 0.f;
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           const uint32_t mkw = c == 0 ? mk0 : c == 1 ? mk1 : c == 2 ? mk2 : mk3;
-          epilogue_chunk(g, rbase, row_ok, m, nt * BN + c * 32, sp, mt, ew, lane, v, mkw,
+          epilogue_chunk<EK>(g, roff, sro, m, nt * BN + c * 32, mt, ew, lane, v, mkw,
                          cta_colsum ? &csum[c * 32 + lane] : nullptr, ostage);
         }
       }

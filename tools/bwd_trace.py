@@ -33,3 +33,11 @@ for name, a, bb in (("prod", 0, 1), ("mma", 2, 3), ("epi", 4, 5)):
     d = t[:, :, bb] - t[:, :, a]
     iv = t[:, 1:, a] - t[:, :-1, a]
     print(f"  {name}: median duration {np.nanmedian(d)/1e3:.3f} us, median start-to-start {np.nanmedian(iv)/1e3:.3f} us")
+b = 0
+for i in range(int(np.sum(~np.isnan(t[b, :, 0])))):
+    e = t[b, i]
+    print(f"  tile {i:3d}: prod {e[0]/1e3:7.2f}-{e[1]/1e3:7.2f} mma {e[2]/1e3:7.2f}-{e[3]/1e3:7.2f}  epi {e[4]/1e3:7.2f}-{e[5]/1e3:7.2f} us")
+first = np.nanmin(t[:, :, 0], axis=1)
+last = np.nanmax(t[:, :, 5], axis=1)
+print(f"  CTA first prod event: min {np.nanmin(first)/1e3:.2f} median {np.nanmedian(first)/1e3:.2f} max {np.nanmax(first)/1e3:.2f} us")
+print(f"  CTA last epi end:     min {np.nanmin(last)/1e3:.2f} median {np.nanmedian(last)/1e3:.2f} max {np.nanmax(last)/1e3:.2f} us")
