@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <math.h>
+#include <utility>
 
 #include "../../include/beast_b200.h"
 
@@ -111,6 +112,36 @@ BP_DEVICE T warp_sum(T v) {
 
 BP_DEVICE void set_status(unsigned* status, unsigned bits) {
   if (status && bits) atomicOr(status, bits);
+}
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  The learner-step kernels are launched with
+// programmatic stream serialization (launch_pdl below): each CTA first signals that the
+// next kernel may launch (pdl_trigger), sets up its shared memory / barriers / TMEM, and
+// then waits in pdl_wait() until the previous kernel has completed and its writes are
+// visible; every global read of an earlier kernel's output comes after pdl_wait().  The
+// next kernel's prologue thus overlaps this kernel's tail.  Both are no-ops for a normal
+// launch.  EVERY kernel of the chain executes pdl_wait() (completion is transitive).
+// ---------------------------------------------------------------------------
+BP_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+BP_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+bool pdl_enabled();  // env BP_PDL=0 disables (A/B)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace bp

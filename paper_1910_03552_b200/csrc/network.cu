@@ -144,7 +144,7 @@ static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUten
     }
     attr = true;
   }
-  kern<<<g.splits, Cfg::THREADS, Cfg::SMEM, s>>>(g, tx, ty);
+  launch_pdl(kern, dim3(g.splits), dim3(Cfg::THREADS), Cfg::SMEM, s, g, tx, ty);
   return check_launch("umma_wgrad_win_kernel");
 }
 template <int BN, int AM, int BM, int BSWZ, bool BRES = false, int AW = 0, int AU8 = 0, int EK = EPK_GEN>
@@ -191,7 +191,7 @@ static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensor
   }
   const int tiles = g.m_tiles * g.n_tiles * g.splits;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, ta, tb);
+  launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, g, ta, tb);
   return check_launch("umma_gemm_kernel");
 }
 
@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
                                                    __nv_bfloat16* __restrict__ whf, const float* __restrict__ reward,
                                                    const int64_t* __restrict__ last_action,
                                                    __nv_bfloat16* __restrict__ core, int n, int A) {
+  pdl_wait();
   if (blockIdx.x < 36) {
     const int core_w = 513 + A;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += 36 * blockDim.x) {
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
 // G [N][64] bf16 = [d_logits (A) | d_baseline | 0 ...]
 __global__ void pack_g_kernel(const float* __restrict__ dlog, const float* __restrict__ dbase,
                               __nv_bfloat16* __restrict__ G, int n, int A) {
+  pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 8-col chunk)
   if (i >= (long long)n * 8) return;
   const int row = (int)(i >> 3), c0 = (int)(i & 7) * 8;
@@ -379,6 +381,7 @@ BP_DEVICE void fin_store(const FinArgs& a, const FinJob& j, long long i, float s
 // thread per output.  Column-sum jobs (thousands of partials, few outputs): one block per
 // output, fixed strided split + fixed shared-memory tree.  All deterministic.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinArgs a) {
+  pdl_wait();
   const FinJob& j = a.job[blockIdx.y];
   if (j.kind == 1) {
     __shared__ float red[256];
@@ -672,9 +675,9 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
   if (conv1_u8()) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
-    prep_kernel<<<36 + (n * 64 + 511) / 512, 512, 0, s>>>(params + off[P_WP], params + off[P_BP], params + off[P_WV],
-                                                          params + off[P_BV], bf(net->whf), reward, last_action,
-                                                          bf(net->core), n, A);
+    launch_pdl(prep_kernel, dim3(36 + (n * 64 + 511) / 512), dim3(512), 0, s, params + off[P_WP],
+               params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf), reward, last_action,
+               bf(net->core), n, A);
     if ((rc = check_launch("prep_kernel"))) return rc;
   } else {
     frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
@@ -868,7 +871,8 @@ static int heads_backward(const BpAtariNet* net, int n, const float* d_logits, c
                           const NetPlan& P, float* ws, float* dh_f32, cudaStream_t s) {
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
-  pack_g_kernel<<<(n * 8 + 255) / 256, 256, 0, s>>>(d_logits, d_baseline, bf(net->g), n, net->num_actions);
+  launch_pdl(pack_g_kernel, dim3((n * 8 + 255) / 256), dim3(256), 0, s, d_logits, d_baseline, bf(net->g), n,
+             net->num_actions);
   if ((rc = check_launch("pack_g_kernel"))) return rc;
   CUtensorMap ta, tb;
   if ((rc = make_tmap(&ta, net->g, n, 64, 64, 128, 128))) return rc;
@@ -1152,7 +1156,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     f.bp_grad = grads + off[P_BP];
     f.wv_grad = grads + off[P_WV];
     f.bv_grad = grads + off[P_BV];
-    finalize_kernel<<<dim3(4 * g_num_sms, k), 256, 0, s>>>(f);
+    launch_pdl(finalize_kernel, dim3(4 * g_num_sms, k), dim3(256), 0, s, f);
     if ((rc = check_launch("finalize_kernel"))) return rc;
   }
   return BP_OK;

@@ -15,6 +15,7 @@ __global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restr
                                                             double* __restrict__ out,
                                                             double* __restrict__ partials,
                                                             unsigned* __restrict__ counter) {
+  pdl_wait();
   const int64_t tid = (int64_t)blockIdx.x * kOptThreads + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kOptThreads;
   float acc = 0.f;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kOptThreads)
                    const float* __restrict__ lr_dev, float alpha, float eps, int write_grads,
                    float* __restrict__ norm_out, __nv_bfloat16* __restrict__ mirror,
                    unsigned* status) {
+  pdl_wait();
   const ClipScale cs = clip_scale(sumsq, max_norm, mode);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (norm_out) *norm_out = (float)sqrt(*sumsq);
@@ -162,7 +164,7 @@ extern "C" int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* work
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + 256);
   int64_t want = (n / 4 + kOptThreads - 1) / kOptThreads;
   int grid = (int)(want < 1 ? 1 : (want > kSumsqBlocks ? kSumsqBlocks : want));
-  sumsq_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(x, n, sumsq, partials, counter);
+  launch_pdl(sumsq_kernel, dim3(grid), dim3(kOptThreads), 0, (cudaStream_t)stream, x, n, sumsq, partials, counter);
   return check_launch("sumsq_kernel");
 }
 
@@ -177,8 +179,8 @@ extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_av
   }
   int64_t want = (n / 4 + kOptThreads - 1) / kOptThreads;
   int grid = (int)(want < 1 ? 1 : (want > 8 * 148 ? 8 * 148 : want));
-  rmsprop_kernel<<<grid, kOptThreads, 0, (cudaStream_t)stream>>>(
-      params, grads, square_avg, n, sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps,
-      write_clipped_grads, norm_out, reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status);
+  launch_pdl(rmsprop_kernel, dim3(grid), dim3(kOptThreads), 0, (cudaStream_t)stream, params, grads, square_avg, n,
+             sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps, write_clipped_grads, norm_out,
+             reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status);
   return check_launch("rmsprop_kernel");
 }

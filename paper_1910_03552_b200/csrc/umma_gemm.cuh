@@ -599,6 +599,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the previous kernel's outputs (every global read below)
 
   const int ntiles = g.m_tiles * g.n_tiles * g.splits;
   // Warps 0 (TMA producer) and 1 (MMA issuer) run their loops converged with
@@ -733,6 +734,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       if (lane == 0) trace_ev(g, ti, 3);
       if (++acc == C::ACC) { acc = 0; aphase ^= 1; }
     }
+    pdl_trigger();  // every MMA of this CTA issued: the next kernel may start launching
   } else if (AU8 > 0 && warp >= C::CONV_WARP0) {
     // converters: raw stage -> swizzled bf16 window in the A ring (one tile per stage)
     const int c = threadIdx.x - 32 * C::CONV_WARP0;
@@ -993,6 +995,7 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the previous kernel's outputs (every global read below)
   const uint32_t stage_tx = (AU8 ? 0 : g.a_cb * g.win_rows * 128) + C::B_BYTES;
 
   if (warp == 0) {
@@ -1079,6 +1082,7 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
       if (sm100::elect_one()) sm100::umma_commit(tfull);
       __syncwarp();
     }
+    pdl_trigger();  // every MMA of this CTA issued: the next kernel may start launching
   } else if (AU8 > 0 && warp >= 8) {
     // converters: raw stage -> swizzled bf16 window of the stage (then one arrival per warp)
     const int c = threadIdx.x - 256;

@@ -192,6 +192,7 @@ template <int A, int kBT, bool LOSS>
 __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args g,
                                                    const __grid_constant__ Maps mp) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  pdl_wait();
   constexpr int RS = kBT * A;  // floats per tile row
   const int T = g.T, B = g.B, nch = g.nchunks;
   const Plan P = plan(T, A, kBT);
@@ -533,7 +534,7 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
     if (blocks_env > 0 && blocks_env < per_sm) per_sm = blocks_env;                               \
     const int grid = g.ntiles < per_sm * tma_num_sms() ? g.ntiles : per_sm * tma_num_sms();       \
     if (loss && ws_bytes < 256 + (size_t)grid * 3 * sizeof(double)) return BP_ERR_UNSUPPORTED;    \
-    k<<<grid, threads, P.total, s>>>(g, m);                                                       \
+    launch_pdl(k, dim3(grid), dim3(threads), P.total, s, g, m);                                  \
     return check_launch("vt3_kernel");                                                            \
   }
   if (A == 6) {

@@ -1,0 +1,46 @@
+"""In-graph kernel durations of the cfg1 learner step (CUPTI through torch.profiler):
+per-kernel mean device time over replays and the idle gaps between kernels.
+
+    python tools/graph_kernels.py [REPLAYS]
+"""
+import sys
+import torch
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_1910_03552_b200 import learner, optim  # noqa: E402
+from paper_1910_03552_b200.atari_net import AtariNet  # noqa: E402
+from torch.profiler import profile, ProfilerActivity  # noqa: E402
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+dev = torch.device("cuda")
+T, B, A = 80, 32, 6
+model = AtariNet(num_actions=A, device=dev)
+opt = optim.RMSprop(model.parameters(), lr=0.0006, alpha=0.99, eps=0.01)
+batch = bench.make_batch(T, B, A, dev, seed=1)
+L = learner.FusedLearner(model, bench.FLAGS, T, B)
+for _ in range(4):
+    L.step(batch, opt)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(reps):
+        L.step(batch, opt)
+    torch.cuda.synchronize()
+ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+steps, cur = [], []
+for e in ev:
+    if "prep_kernel" in e.name and cur:
+        steps.append(cur)
+        cur = []
+    cur.append(e)
+steps.append(cur)
+steps = [s for s in steps if s and "prep_kernel" in s[0].name]
+k = len(steps[0])
+print(f"{len(steps)} replays, {k} kernels per step")
+tot = 0.0
+for i in range(k):
+    d = sum(s[i].time_range.elapsed_us() for s in steps if len(s) == k) / len(steps)
+    gap = sum((s[i].time_range.start - s[i - 1].time_range.end) for s in steps if len(s) == k and i > 0) / len(steps)
+    tot += d
+    print(f"{i:3d} {d:8.1f} us  gap-before {gap:6.1f}  {steps[0][i].name[:90]}")
+span = sum(s[-1].time_range.end - s[0].time_range.start for s in steps) / len(steps)
+print(f"sum of kernel times {tot:.1f} us, step span {span:.1f} us")
