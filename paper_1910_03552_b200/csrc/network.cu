@@ -85,6 +85,17 @@ static int conv1_u8_mode() {
   return g_conv1_u8;
 }
 static bool conv1_u8() { return conv1_u8_mode() != 0; }
+// conv1 bias gradient: from the conv2 data-gradient epilogue's column sums (default), or from
+// an all-ones atom in the conv1 window weight gradient (env BP_CONV1_ONES=1; one more M tile of
+// MMAs -- the conv1 weight gradient is bound by the tensor pipe's shared-memory reads)
+static bool conv1_ones() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("BP_CONV1_ONES");
+    v = e && e[0] == '1' ? 1 : 0;
+  }
+  return v == 1;
+}
 
 static void set_window(GemmArgs& g, int taps) {
   int mn = 0, mx = 0;
@@ -131,7 +142,7 @@ static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUten
   using Cfg = WgCfg<BN, BSWZ, NMT, AU8, CB, WR>;
   auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT, AU8, CB, WR>;
   WgArgs g = g0;
-  if (g.win_rows > WR || g.a_cb > Cfg::MAX_CB || g.splits < 1) {
+  if (g.win_rows > WR || g.a_cb > Cfg::MAX_CB || g.splits < 1 || (g.colsum && (BN != 32 || BSWZ != 64))) {
     set_error("wgrad window: %d rows / %d channel blocks unsupported", g.win_rows, g.a_cb);
     return BP_ERR_ARG;
   }
@@ -453,7 +464,7 @@ static void make_plan(int n, int sms, NetPlan* P, bool win) {
   // conv3's 9 taps x 64 channels pad to 5 m-tiles (the 10th atom is the zero atom)
   // window mode: conv1 gets one more m-tile (the all-ones atom -> db1 rows, which spares the
   // conv2 dgrad epilogue its column sums); conv3's 9 taps leave atom 9 free for db3
-  const int M[4] = {win ? 384 : 256, 512, 576, kCoreW};
+  const int M[4] = {win && conv1_ones() ? 384 : 256, 512, 576, kCoreW};
   const int Ns[4] = {32, 64, 64, 64};
   size_t off = 0;
   for (int i = 0; i < 4; ++i) {
@@ -982,7 +993,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.gh = 10; g.gw = 10; g.vh = 10; g.vw = 10;
     g.r_img = 441 * 32; g.r_y = 2 * 21 * 32; g.r_x = 2 * 32;
     g.cdiv = 32; g.cq = 2; g.cs1 = 21 * 32; g.cs2 = 32;
-    g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[0];  // window mode: bias from the wgrad ones atom
+    g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[0];  // window mode: db1 from the conv1 wgrad
     if ((rc = launch_gemm<128, A_KMAJOR, B_MNMAJOR, 128, true, 1, 0, EPK_DGRAD>(g, ta, tb, s))) return rc;
   }
   // weight gradients
@@ -1034,13 +1045,16 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.win_rows = (64 + mx + 7) & ~7;
     g.Mpad = (int)w.Mpad;
     g.N = w.Npad;
-    g.ones_atom = i == 1 ? -1 : nshifts * (xcols / 64);  // the atom after the taps: bias rows
+    // the atom after the taps: bias rows (conv3; conv1 with BP_CONV1_ONES)
+    g.ones_atom = i == 1 || (i == 0 && !conv1_ones()) ? -1 : nshifts * (xcols / 64);
     g.out = ws + w.off;
+    if (i == 0 && !conv1_ones()) g.colsum = ws + P.cs_off[0];  // db1: the column-sum warp
     int r;
     if ((r = make_tmap(&ta, X, xrows, xcols, 64, g.win_rows, 128))) return r;
     if (ncols == 32) {
       if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
-      return launch_wgrad_win<32, 64, 3, 0, 1, 88>(g, ta, tb, s);
+      return conv1_ones() ? launch_wgrad_win<32, 64, 3, 0, 1, 88>(g, ta, tb, s)
+                          : launch_wgrad_win<32, 64, 2, 0, 1, 88>(g, ta, tb, s);
     }
     if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
     return i == 1 ? launch_wgrad_win<64, 128, 4, 0, 2, 80>(g, ta, tb, s)
@@ -1068,14 +1082,15 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       g.win_rows = (64 + 22 + 7) & ~7;
       g.Mpad = (int)w.Mpad;
       g.N = w.Npad;
-      g.ones_atom = wgrad_window() ? 4 : -1;
+      g.ones_atom = wgrad_window() && conv1_ones() ? 4 : -1;
       g.out = ws + w.off;
+      if (wgrad_window() && !conv1_ones()) g.colsum = ws + P.cs_off[0];  // db1: the column-sum warp
       g.u8 = src->frames;
       g.u8_index = src->plane_index;
       g.u8_planes = src->num_planes;
       g.u8_rows = (long long)n * 441;
       if ((rc = make_tmap(&tb, net->d_pre1, (long long)n * 441, 32, 32, 64, 64))) return rc;
-      if ((rc = wgrad_window() ? launch_wgrad_win<32, 64, 3, 1, 1, 88>(g, tb, tb, s)
+      if ((rc = wgrad_window() && conv1_ones() ? launch_wgrad_win<32, 64, 3, 1, 1, 88>(g, tb, tb, s)
                                : launch_wgrad_win<32, 64, 2, 1, 1, 88>(g, tb, tb, s)))
         return rc;
     } else if (wgrad_window()) {
@@ -1133,15 +1148,18 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       const WgPlan& w = P.wg[3];
       f.job[k++] = {ws + w.off, nullptr, 2, w.splits, 513 + A + 1, A + 1, w.Npad, w.Mpad, 1.f};
     }
-    // biases.  Window mode: db1 and db3 are the all-ones-atom rows of the conv1 / conv3
-    // weight-gradient partials (sums over rows of the bf16 dY), split-reduced like the weights;
-    // db2 and dbfc come from the conv3 / heads dgrad epilogue column sums.  Per-tap mode: db1 from conv2 dgrad (width 128 = 4 groups of 32), db2, db3
-    // (3136 = 49 x 64), dbfc from their epilogue column sums.
+    // biases.  Window mode: db3 (and db1 with BP_CONV1_ONES) are the all-ones-atom rows of the
+    // conv3 (conv1) weight-gradient partials (sums over rows of the bf16 dY), split-reduced like
+    // the weights.  Otherwise from the data-gradient epilogue column sums: db1 from conv2 dgrad
+    // (width 128 = 4 groups of 32), db2 from conv3 dgrad, db3 from fc dgrad (3136 = 49 x 64),
+    // dbfc from heads dgrad.
     const int pb[4] = {P_B1, P_B2, P_B3, P_BFC};
     const int C[4] = {32, 64, 64, 512};
     const int ones_row[3] = {4 * 64, 0, 9 * 64};
     for (int i = 0; i < 4; ++i) {
-      if ((i == 0 || i == 2) && wgrad_window()) {
+      if (i == 0 && wgrad_window() && !conv1_ones()) {  // the conv1 wgrad's per-CTA dY column sums
+        f.job[k++] = {ws + P.cs_off[0], grads + off[pb[0]], 1, P.wg[0].splits, 1, C[0], 0, 0, 1.f};
+      } else if ((i == 2 || (i == 0 && conv1_ones())) && wgrad_window()) {
         const WgPlan& w = P.wg[i];
         f.job[k++] = {ws + w.off + (size_t)ones_row[i] * w.Npad, grads + off[pb[i]], 0, w.splits, 1, C[i],
                       w.Npad, w.Mpad, 1.f};

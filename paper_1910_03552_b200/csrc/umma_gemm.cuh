@@ -920,6 +920,9 @@ struct WgArgs {
   int ones_atom;  // atom index holding all ones (its D rows = column sums of dY: the bias
                   // gradient), -1 = none; atoms past the taps and the ones atom are zero
   float* out;
+  // optional (BN == 32, BSWZ == 64): column sums of the CTA's dY rows (the bias gradient),
+  // colsum[blockIdx.x][BN], summed by the otherwise idle warp 3 from the staged dY boxes
+  float* colsum;
   unsigned long long* trace;
   int trace_tiles;
   // AU8 (conv1): the X windows are converted on chip from u8 frames (see GemmArgs)
@@ -979,7 +982,7 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
     sm100::tma_prefetch_desc(&tmY);
     for (int s = 0; s < C::STAGES; ++s) {
       sm100::mbar_init(&full[s], AU8 ? 1 + kConvWarps : 1);  // AU8: + one arrival per converter warp
-      sm100::mbar_init(&empty[s], 1);
+      sm100::mbar_init(&empty[s], g.colsum ? 2 : 1);         // + the column-sum warp
     }
     sm100::mbar_init(tfull, 1);
     if constexpr (AU8 > 0) {
@@ -1104,6 +1107,50 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
         if (++rs == kRawStages) { rs = 0; rph ^= 1; }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
+    }
+  } else if (warp == 3 && g.colsum) {
+    // bias gradient: column sums of the dY boxes (64 rows x 32 bf16, 64B-swizzled rows: the
+    // 16-byte chunk j of row r sits at r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); lane l sums
+    // chunk j = l & 3 of rows l / 4 + 8 i, i.e. channels 8j .. 8j + 7, in f32
+    float cs[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cs[i] = 0.f;
+    const int j = lane & 3, r0 = lane >> 2;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
+      const int kb0 = sp * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&full[stage], phase);
+        const uint32_t sb = after_wait(sm100::smem_addr(ring + stage * C::STAGE + C::MAX_CB * C::WIN_BYTES));
+        uint32_t w[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 8 * i;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                       : "r"(sb + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)));
+        }
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&empty[stage]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            cs[2 * q] += __uint_as_float(w[i][q] << 16);
+            cs[2 * q + 1] += __uint_as_float(w[i][q] & 0xFFFF0000u);
+          }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    // lanes with the same chunk j (l = j + 4 k): fixed-order butterfly over k
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
+    if (lane < 4) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g.colsum[(size_t)blockIdx.x * BN + 8 * j + i] = cs[i];
     }
   } else if (warp >= 4 && warp < 8) {
     const int ew = warp - 4;
