@@ -142,7 +142,7 @@ static int launch_wgrad_win(const WgArgs& g0, const CUtensorMap& tx, const CUten
   using Cfg = WgCfg<BN, BSWZ, NMT, AU8, CB, WR>;
   auto kern = umma_wgrad_win_kernel<BN, BSWZ, NMT, AU8, CB, WR>;
   WgArgs g = g0;
-  if (g.win_rows > WR || g.a_cb > Cfg::MAX_CB || g.splits < 1 || (g.colsum && (BN != 32 || BSWZ != 64))) {
+  if (g.win_rows > WR || g.a_cb > Cfg::MAX_CB || g.splits < 1 || (g.colsum && !((BN == 32 && BSWZ == 64) || (BN == 64 && BSWZ == 128)))) {
     set_error("wgrad window: %d rows / %d channel blocks unsupported", g.win_rows, g.a_cb);
     return BP_ERR_ARG;
   }
@@ -969,7 +969,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.out = net->d_pre2;
     g.gh = 9; g.gw = 9; g.vh = 9; g.vw = 9;
     g.r_img = 100 * 64; g.r_y = 10 * 64; g.r_x = 64;
-    g.colsum = ws + P.cs_off[1];  // db2
+    g.colsum = wgrad_window() ? nullptr : ws + P.cs_off[1];  // db2 (window mode: from the conv2 wgrad)
     if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, true, 1, 0, EPK_DGRAD>(g, ta, tb, s))) return rc;
   }
   // conv2 dgrad: d_pre1 (conv1 21x21 grid) = sum_taps d_pre2[m - off] W2_tap^T * (X1 > 0), inverse s2d
@@ -1049,6 +1049,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.ones_atom = i == 1 || (i == 0 && !conv1_ones()) ? -1 : nshifts * (xcols / 64);
     g.out = ws + w.off;
     if (i == 0 && !conv1_ones()) g.colsum = ws + P.cs_off[0];  // db1: the column-sum warp
+    if (i == 1) g.colsum = ws + P.cs_off[1];                     // db2: the column-sum warp
     int r;
     if ((r = make_tmap(&ta, X, xrows, xcols, 64, g.win_rows, 128))) return r;
     if (ncols == 32) {
@@ -1148,17 +1149,19 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       const WgPlan& w = P.wg[3];
       f.job[k++] = {ws + w.off, nullptr, 2, w.splits, 513 + A + 1, A + 1, w.Npad, w.Mpad, 1.f};
     }
-    // biases.  Window mode: db3 (and db1 with BP_CONV1_ONES) are the all-ones-atom rows of the
-    // conv3 (conv1) weight-gradient partials (sums over rows of the bf16 dY), split-reduced like
-    // the weights.  Otherwise from the data-gradient epilogue column sums: db1 from conv2 dgrad
-    // (width 128 = 4 groups of 32), db2 from conv3 dgrad, db3 from fc dgrad (3136 = 49 x 64),
-    // dbfc from heads dgrad.
+    // biases.  Window mode: db1 and db2 are the column-sum warp's per-CTA sums of the bf16 dY
+    // boxes in the conv1 / conv2 weight-gradient kernels; db3 (and db1 with BP_CONV1_ONES) the
+    // all-ones-atom rows of the conv3 (conv1) weight-gradient partials, split-reduced like the
+    // weights.  Per-tap mode: from the data-gradient epilogue column sums: db1 from conv2 dgrad
+    // (width 128 = 4 groups of 32), db2 from conv3 dgrad, db3 from fc dgrad (3136 = 49 x 64).
+    // dbfc always from the heads dgrad.
     const int pb[4] = {P_B1, P_B2, P_B3, P_BFC};
     const int C[4] = {32, 64, 64, 512};
     const int ones_row[3] = {4 * 64, 0, 9 * 64};
     for (int i = 0; i < 4; ++i) {
-      if (i == 0 && wgrad_window() && !conv1_ones()) {  // the conv1 wgrad's per-CTA dY column sums
-        f.job[k++] = {ws + P.cs_off[0], grads + off[pb[0]], 1, P.wg[0].splits, 1, C[0], 0, 0, 1.f};
+      if ((i == 0 && wgrad_window() && !conv1_ones()) || (i == 1 && wgrad_window())) {
+        // the conv1 / conv2 window wgrad's per-CTA dY column sums
+        f.job[k++] = {ws + P.cs_off[i], grads + off[pb[i]], 1, P.wg[i].splits, 1, C[i], 0, 0, 1.f};
       } else if ((i == 2 || (i == 0 && conv1_ones())) && wgrad_window()) {
         const WgPlan& w = P.wg[i];
         f.job[k++] = {ws + w.off + (size_t)ones_row[i] * w.Npad, grads + off[pb[i]], 0, w.splits, 1, C[i],

@@ -920,7 +920,8 @@ struct WgArgs {
   int ones_atom;  // atom index holding all ones (its D rows = column sums of dY: the bias
                   // gradient), -1 = none; atoms past the taps and the ones atom are zero
   float* out;
-  // optional (BN == 32, BSWZ == 64): column sums of the CTA's dY rows (the bias gradient),
+  // optional (BN == 32 / BSWZ == 64 or BN == 64 / BSWZ == 128): column sums of the CTA's dY
+  // rows (the bias gradient),
   // colsum[blockIdx.x][BN], summed by the otherwise idle warp 3 from the staged dY boxes
   float* colsum;
   unsigned long long* trace;
@@ -1109,13 +1110,16 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
       }
     }
   } else if (warp == 3 && g.colsum) {
-    // bias gradient: column sums of the dY boxes (64 rows x 32 bf16, 64B-swizzled rows: the
-    // 16-byte chunk j of row r sits at r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); lane l sums
-    // chunk j = l & 3 of rows l / 4 + 8 i, i.e. channels 8j .. 8j + 7, in f32
+    // bias gradient: column sums of the dY boxes (64 rows x BN bf16; BN = 32: 64B-swizzled rows,
+    // the 16-byte chunk j of row r at r * 64 + ((j ^ ((r >> 1) & 3)) << 4); BN = 64: 128B rows,
+    // at r * 128 + ((j ^ (r & 7)) << 4)).  Lane l sums chunk j = l % CPR (channels 8j .. 8j + 7)
+    // of rows l / CPR + RPI i, in f32
+    constexpr int CPR = BN * 2 / 16, RPI = 32 / CPR, NI = 64 / RPI;
+    static_assert((BN == 32 && BSWZ == 64) || (BN == 64 && BSWZ == 128), "column-sum warp layout");
     float cs[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) cs[i] = 0.f;
-    const int j = lane & 3, r0 = lane >> 2;
+    const int j = lane % CPR, r0 = lane / CPR;
     int stage = 0;
     uint32_t phase = 0;
     for (int sp = blockIdx.x; sp < g.splits; sp += gridDim.x) {
@@ -1123,18 +1127,19 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         sm100::mbar_wait(&full[stage], phase);
         const uint32_t sb = after_wait(sm100::smem_addr(ring + stage * C::STAGE + C::MAX_CB * C::WIN_BYTES));
-        uint32_t w[8][4];
+        uint32_t w[NI][4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = r0 + 8 * i;
+        for (int i = 0; i < NI; ++i) {
+          const int r = r0 + RPI * i;
+          const uint32_t a = BN == 32 ? sb + r * 64 + ((j ^ ((r >> 1) & 3)) << 4) : sb + r * 128 + ((j ^ (r & 7)) << 4);
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                        : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
-                       : "r"(sb + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)));
+                       : "r"(a));
         }
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&empty[stage]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < NI; ++i)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             cs[2 * q] += __uint_as_float(w[i][q] << 16);
@@ -1143,12 +1148,12 @@ __global__ void __launch_bounds__(WgCfg<BN, BSWZ, NMT, AU8, CB, WR>::THREADS, 1)
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    // lanes with the same chunk j (l = j + 4 k): fixed-order butterfly over k
+    // lanes with the same chunk j (l = j + CPR k): fixed-order butterfly over k
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1)
+    for (int o = CPR; o < 32; o <<= 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
-    if (lane < 4) {
+    if (lane < CPR) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) g.colsum[(size_t)blockIdx.x * BN + 8 * j + i] = cs[i];
     }

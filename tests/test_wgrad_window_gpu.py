@@ -1,8 +1,9 @@
 """Conv weight gradients through the window kernel (one X window + dY box per K-block, every
 M atom an MN-major view with LBO = the distance to its partner atom, zero atom for conv3's
 odd tap count) vs the per-tap-box GEMM path: same products, different split-K plan, so the
-gradients agree to f32 summation-order tolerance (rel 1e-5); the conv1/conv3 biases come from
-an all-ones atom over the bf16 dY in window mode (rel 5e-3)."""
+gradients agree to f32 summation-order tolerance (rel 1e-5); in window mode the conv1/conv2
+biases are column sums of the bf16 dY boxes (column-sum warp) and the conv3 bias comes from an
+all-ones atom over the bf16 dY (rel 5e-3)."""
 import pytest
 import torch
 
@@ -35,8 +36,8 @@ def test_wgrad_window_matches_per_tap_path(n):
     names = [k for k, _ in net.named_parameters()]
     for name, a, b in zip(names, net._split(grads[0]), net._split(grads[1])):
         err = float((a - b).norm() / b.norm().clamp_min(1e-30))
-        # conv1 / conv3 biases: window mode sums the bf16-stored dY through an all-ones atom;
+        # conv biases: window mode sums the bf16-stored dY (column-sum warp / all-ones atom);
         # the per-tap path sums the f32 epilogue values (bf16 rounding, well inside the 2e-2
         # gradient tolerance of the bf16 network)
-        tol = 5e-3 if name in ("conv1.bias", "conv3.bias") else 1e-5
+        tol = 5e-3 if name in ("conv1.bias", "conv2.bias", "conv3.bias") else 1e-5
         assert err <= tol, (name, err)
