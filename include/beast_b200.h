@@ -297,6 +297,13 @@ int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1
  * logits [n][A] f32 -> actions [n] int64. */
 int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
                           int64_t* actions, void* stream);
+/* Learner-step stats read-back (monobeast learn() stats: losses + episode returns of the
+ * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
+ * (nullable) into out = [32 B losses | tb B done | tb * 4 B returns] in one launch.  out may
+ * be device memory or pinned host memory (written through its unified-address mapping: the
+ * step's result reaches the host without a separate copy). */
+int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
+                  void* out, void* stream);
 /* Shifted-tap GEMM test entry (the convolution form of the engine):
  * C[m][n] = sum_t sum_c A[m + offs[t]][c] * B[n][t*Cin + c]; window_mode 0 = one TMA box
  * per tap, 1 / 2 = one shared window per channel block (descriptor base offset 0 / row&7).

@@ -146,9 +146,48 @@ __global__ void __launch_bounds__(kOptThreads)
   }
 }
 
+// stats read-back buffer: [losses 4 x f64 | done tb x u8 | returns tb x f32 at byte offset
+// 32 + tb (byte stores when that is not 4-byte aligned)]; one element per thread
+__global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restrict__ losses,
+                                                         const uint8_t* __restrict__ done,
+                                                         const float* __restrict__ ret, int tb,
+                                                         uint8_t* __restrict__ out) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 4) reinterpret_cast<double*>(out)[i] = losses[i];
+  if (i >= tb) return;
+  out[32 + i] = done[i] ? 1 : 0;
+  if (ret) {
+    uint8_t* o = out + 32 + tb;
+    if ((tb & 3) == 0) {
+      reinterpret_cast<float*>(o)[i] = ret[i];
+    } else {
+      const uint32_t v = __float_as_uint(ret[i]);
+      o[4 * i] = (uint8_t)v;
+      o[4 * i + 1] = (uint8_t)(v >> 8);
+      o[4 * i + 2] = (uint8_t)(v >> 16);
+      o[4 * i + 3] = (uint8_t)(v >> 24);
+    }
+  }
+  // (out may be mapped pinned host memory: the host reads it after an event synchronize on
+  // the stream, which orders these writes)
+}
+
 }  // namespace bp
 
 using namespace bp;
+
+extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
+                             void* out, void* stream) {
+  if (!losses || !done || !out || tb < 0) {
+    set_error("pack_stats: bad args");
+    return BP_ERR_ARG;
+  }
+  const int n = tb > 4 ? tb : 4;
+  launch_pdl(pack_stats_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, losses, done,
+             episode_return, tb, reinterpret_cast<uint8_t*>(out));
+  return check_launch("pack_stats_kernel");
+}
 
 extern "C" size_t bp_sumsq_workspace_bytes(int64_t n) {
   (void)n;

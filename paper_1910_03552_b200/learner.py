@@ -58,10 +58,10 @@ class FusedLearner:
         self.d_logits = torch.zeros(self.n, A, device=dev)  # row T stays zero
         self.d_baseline = torch.zeros(self.n, device=dev)
         self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
-        # stats read-back: losses + done[1:] + episode_return[1:] in ONE pinned D2H per step
+        # stats read-back: losses + done[1:] + episode_return[1:], written by one kernel straight
+        # into pinned (device-mapped) host memory: one device->host transfer per step, no copy node
         self._stats_host = torch.empty(4 * 8 + unroll_length * batch_size * 5, dtype=torch.uint8,
                                        pin_memory=True)
-        self._stats_dev = torch.empty_like(self._stats_host, device=dev)
         self._stats_event = torch.cuda.Event()
         # numpy views of the pinned read-back buffer (no per-step tensor/numpy conversions)
         tb = unroll_length * batch_size
@@ -205,18 +205,22 @@ class FusedLearner:
         return self.losses
 
     def _pack_stats(self, batch, losses):
-        """Loss vector, done[1:] and episode_return[1:] -> one device buffer -> ONE pinned D2H
-        copy.  Part of the step (and of its CUDA graph)."""
+        """Loss vector, done[1:] and episode_return[1:] -> the pinned read-back buffer, written
+        by one kernel through the device mapping of the pinned host memory (unified virtual
+        addressing).  Part of the step (and of its CUDA graph)."""
         T, B = self.T, self.B
         tb = T * B
-        dev_buf, host = self._stats_dev, self._stats_host
-        dev_buf[:32].view(torch.float64).copy_(losses)
-        dev_buf[32:32 + tb].copy_(batch["done"][1:].reshape(tb).view(torch.uint8)
-                                  if batch["done"].dtype == torch.bool else batch["done"][1:].reshape(tb))
+        host = self._stats_host
+        done = batch["done"][1:].reshape(tb)
+        done = done.view(torch.uint8) if done.dtype == torch.bool else done.to(torch.uint8)
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
         if ep is not None:
-            dev_buf[32 + tb:].view(torch.float32).copy_(ep[1:].reshape(tb))
-        host.copy_(dev_buf, non_blocking=True)
+            ep = ep[1:].reshape(tb)
+            if ep.dtype != torch.float32 or not ep.is_contiguous():
+                ep = ep.float().contiguous()
+        losses = losses if losses.dtype == torch.float64 and losses.is_contiguous() else losses.double().contiguous()
+        N.check(N.lib().bp_pack_stats(losses.data_ptr(), done.data_ptr(), ep.data_ptr() if ep is not None else None,
+                                      tb, host.data_ptr(), N.stream_handle(losses.device)), "bp_pack_stats")
 
     def stats(self, batch, losses=None):
         """Upstream learn() stats dict from the step's packed read-back (one sync)."""
