@@ -297,6 +297,11 @@ int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1
  * logits [n][A] f32 -> actions [n] int64. */
 int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
                           int64_t* actions, void* stream);
+/* Infeed slot refill (DeviceInfeed.put; the reference stacks rollouts on the host,
+ * rollout.py:116-144): on `stream`, wait for wait_event (nullable: the consumer released the
+ * slot), copy `bytes` from pinned host src to device dst, record ready_event. */
+int bp_infeed_put(void* dst, const void* src, size_t bytes, void* stream, void* wait_event,
+                  void* ready_event);
 /* Learner-step stats read-back (monobeast learn() stats: losses + episode returns of the
  * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
  * (nullable) into out = [32 B losses | tb B done | tb * 4 B returns] in one launch.  out may

@@ -293,6 +293,11 @@ class DeviceInfeed:
         self.events = [torch.cuda.Event() for _ in range(depth)]
         self.freed = [torch.cuda.Event() for _ in range(depth)]
         self.stream = torch.cuda.Stream(device=self.device)
+        # raw handles for the one-call refill (bp_infeed_put); torch creates an event's
+        # CUDA handle at its first record
+        for ev in self.events + self.freed:
+            ev.record(self.stream)
+        self._stream_h = self.stream.cuda_stream
         self.head = 0  # next slot to fill
         self.tail = 0  # next slot to consume
         self.bytes_per_batch = sum(v.numel() * v.element_size() for v in like.values())
@@ -314,6 +319,15 @@ class DeviceInfeed:
 
     def put(self, host_batch: dict) -> None:
         slot = self.head % self.depth
+        flat = host_batch.get("__flat__")
+        if flat is not None and flat.numel() == self.packed_bytes and flat.is_pinned():
+            # packed pinned batch: wait-for-release + one H2D copy + ready event in one C call
+            N.check(N.lib().bp_infeed_put(self.flat[slot].data_ptr(), flat.data_ptr(), self.packed_bytes,
+                                          self._stream_h,
+                                          self.freed[slot].cuda_event if self.head >= self.depth else None,
+                                          self.events[slot].cuda_event), "bp_infeed_put")
+            self.head += 1
+            return
         with torch.cuda.stream(self.stream):
             if self.head >= self.depth:
                 self.stream.wait_event(self.freed[slot])  # consumer done with this slot
