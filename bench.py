@@ -396,7 +396,7 @@ def main():
                 if i + 1 < nsteps:
                     infeed.put(host[(i + 1) % 2])
                 out = learner.learn(FLAGS, None, model, b, (), opt, None, process_group=pg)
-                infeed.release()
+                # (the next get() releases this slot on the stream: one native call per step)
             return out
 
         e2e_run(6)  # per infeed slot: eager step, graph capture, replay -> timed steps replay only

@@ -302,6 +302,9 @@ int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int 
  * slot), copy `bytes` from pinned host src to device dst, record ready_event. */
 int bp_infeed_put(void* dst, const void* src, size_t bytes, void* stream, void* wait_event,
                   void* ready_event);
+/* Infeed consumer (DeviceInfeed.get / release): on `stream`, record release_event (nullable)
+ * after the work enqueued so far, then wait for ready_event (the next slot's copy). */
+int bp_infeed_get(void* stream, void* release_event, void* ready_event);
 /* Learner-step stats read-back (monobeast learn() stats: losses + episode returns of the
  * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
  * (nullable) into out = [32 B losses | tb B done | tb * 4 B returns] in one launch.  out may

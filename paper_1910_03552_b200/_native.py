@@ -56,6 +56,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
     "bp_pack_stats": (I, [P, P, P, I, P, P]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),
+    "bp_infeed_get": (I, [P, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),
     "bp_gemm_shift_test": (I, [P, P, P, I, I, I, I, P, I, P, I, P]),
 }

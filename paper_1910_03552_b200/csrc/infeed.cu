@@ -25,3 +25,21 @@ extern "C" int bp_infeed_put(void* dst, const void* src, size_t bytes, void* str
   }
   return BP_OK;
 }
+
+// consumer side: on `stream`, record release_event (nullable: the previously consumed slot is
+// reusable once the work enqueued so far is done), then wait for the next slot's ready_event
+extern "C" int bp_infeed_get(void* stream, void* release_event, void* ready_event) {
+  if (!ready_event) {
+    set_error("infeed_get: bad args");
+    return BP_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (release_event) e = cudaEventRecord((cudaEvent_t)release_event, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, (cudaEvent_t)ready_event, 0);
+  if (e != cudaSuccess) {
+    set_error("infeed_get: %s", cudaGetErrorString(e));
+    return BP_ERR_LAUNCH;
+  }
+  return BP_OK;
+}

@@ -298,6 +298,7 @@ class DeviceInfeed:
         for ev in self.events + self.freed:
             ev.record(self.stream)
         self._stream_h = self.stream.cuda_stream
+        self._released = True
         self.head = 0  # next slot to fill
         self.tail = 0  # next slot to consume
         self.bytes_per_batch = sum(v.numel() * v.element_size() for v in like.values())
@@ -341,14 +342,22 @@ class DeviceInfeed:
         self.head += 1
 
     def get(self) -> dict:
+        """The next filled slot; the current stream waits for its copy.  A slot consumed
+        before and not yet release()d is released first (at this point of the stream)."""
         if self.tail >= self.head:
             raise RuntimeError("DeviceInfeed.get() without a pending put()")
         slot = self.tail % self.depth
-        torch.cuda.current_stream(self.device).wait_event(self.events[slot])
+        prev = (self.tail - 1) % self.depth
+        rel = self.freed[prev].cuda_event if self.tail > 0 and not self._released else None
+        N.check(N.lib().bp_infeed_get(torch.cuda.current_stream(self.device).cuda_stream, rel,
+                                      self.events[slot].cuda_event), "bp_infeed_get")
         self.tail += 1
+        self._released = False
         return self.slots[slot]
 
     def release(self) -> None:
-        """Mark the most recently consumed slot reusable (after its step was enqueued)."""
+        """Mark the most recently consumed slot reusable (after its step was enqueued).
+        Optional: get() releases the previous slot itself."""
         slot = (self.tail - 1) % self.depth
         self.freed[slot].record(torch.cuda.current_stream(self.device))
+        self._released = True

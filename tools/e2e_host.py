@@ -42,7 +42,7 @@ def run(n, record):
         t3 = time.perf_counter()
         L.stats(b)
         t4 = time.perf_counter()
-        infeed.release()
+        infeed.release()  # (optional: get() releases the previous slot itself)
         t5 = time.perf_counter()
         if record:
             for k, v in zip(("get", "put", "step", "stats", "release", "total"),
