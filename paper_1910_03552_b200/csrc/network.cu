@@ -411,37 +411,40 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
     }
     return;
   }
-  // split-K: one thread per output; consecutive threads read consecutive partial
-  // columns (coalesced), the split loop is unrolled for memory-level parallelism
+  // split-K: a block takes 32 consecutive outputs (lane = output: coalesced partial rows);
+  // its 8 warps split the partials (warp w sums splits w, w + 8, ...; 8 loads in flight per
+  // lane), then warp 0 adds the 8 warp sums in a fixed order.  The one-thread-per-output form
+  // had 16 loads in flight on ~2 blocks per SM and was latency-bound.
+  __shared__ float red8[8][32];
   const long long total = (long long)j.M * j.N;
   const long long pstride = j.Mpad * j.Npad;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long m = i / j.N, n = i % j.N;
-    const float* p = j.partial + m * j.Npad + n;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int r = 0;
-    // 16 loads in flight per thread; the sums keep the fixed r mod 4 order
-    for (; r + 16 <= j.splits; r += 16) {
-      float v[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * 32; base < total; base += (long long)gridDim.x * 32) {
+    const long long i = base + lane;
+    float s = 0.f;
+    if (i < total) {
+      const long long m = i / j.N, n = i % j.N;
+      const float* p = j.partial + m * j.Npad + n;
+      for (int r = warp; r < j.splits; r += 64) {
+        float v[8];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = __ldcs(p + (long long)(r + q) * pstride);
+        for (int q = 0; q < 8; ++q) {
+          const int rr = r + 8 * q;
+          v[q] = rr < j.splits ? __ldcs(p + (long long)rr * pstride) : 0.f;
+        }
 #pragma unroll
-      for (int q = 0; q < 16; q += 4) {
-        s0 += v[q];
-        s1 += v[q + 1];
-        s2 += v[q + 2];
-        s3 += v[q + 3];
+        for (int q = 0; q < 8; ++q) s += v[q];
       }
     }
-    for (; r + 4 <= j.splits; r += 4) {
-      s0 += p[(long long)r * pstride];
-      s1 += p[(long long)(r + 1) * pstride];
-      s2 += p[(long long)(r + 2) * pstride];
-      s3 += p[(long long)(r + 3) * pstride];
+    red8[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < total) {
+      float t = red8[0][lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) t += red8[w][lane];
+      fin_store(a, j, i, t);
     }
-    for (; r < j.splits; ++r) s0 += p[(long long)r * pstride];
-    fin_store(a, j, i, (s0 + s1) + (s2 + s3));
+    __syncthreads();
   }
 }
 
