@@ -9,7 +9,10 @@
 namespace bp {
 
 constexpr int kOptThreads = 256;
-constexpr int kSumsqBlocks = 8 * 148;
+#ifndef BP_SUMSQ_BLOCKS
+#define BP_SUMSQ_BLOCKS (2 * 148)  // A/B vs 4 and 8 x 148: within noise
+#endif
+constexpr int kSumsqBlocks = BP_SUMSQ_BLOCKS;
 
 __global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restrict__ x, int64_t n,
                                                             double* __restrict__ out,
