@@ -55,3 +55,22 @@ torch.cuda.synchronize()
 run(steps, True)
 for k, v in ph.items():
     print(f"{k:8s} median {statistics.median(v):8.1f} us  mean {statistics.mean(v):8.1f} us")
+
+# host-only cost of stats() and learn() pieces with the GPU idle
+infeed.put(host[0])
+b = infeed.get()
+L.step(b, opt, None, ())
+torch.cuda.synchronize()
+ts = []
+for _ in range(50):
+    t0 = time.perf_counter()
+    L.stats(b)
+    ts.append((time.perf_counter() - t0) * 1e6)
+print(f"stats() with the GPU idle: median {statistics.median(ts):.1f} us")
+ts = []
+for _ in range(50):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L.step(b, opt, None, ())
+    ts.append((time.perf_counter() - t0) * 1e6)
+print(f"step() launch: median {statistics.median(ts):.1f} us")
