@@ -367,12 +367,16 @@ BP_DEVICE float fin_partial(const FinJob& j, long long i, int r) {
   return j.partial[((long long)r * j.Mpad + m) * j.Npad + n];
 }
 
+BP_DEVICE void fin_store_mn(const FinArgs& a, const FinJob& j, int m, int n, float s);
 BP_DEVICE void fin_store(const FinArgs& a, const FinJob& j, long long i, float s) {
   if (j.kind == 1) {
     j.dst[i] = s;
     return;
   }
-  const long long m = i / j.N, n = i % j.N;
+  fin_store_mn(a, j, (int)(i / j.N), (int)(i % j.N), s);
+}
+// split-K outputs (kind 0: conv weights transposed to [Cout][K]; kind 2: heads), element (m, n)
+BP_DEVICE void fin_store_mn(const FinArgs& a, const FinJob& j, int m, int n, float s) {
   s *= j.alpha;
   if (j.kind == 0) {
     j.dst[n * j.M + m] = s;
@@ -388,9 +392,9 @@ BP_DEVICE void fin_store(const FinArgs& a, const FinJob& j, long long i, float s
   }
 }
 
-// Split-K jobs: one warp per output (fixed lane split + fixed shuffle tree) or one
-// thread per output.  Column-sum jobs (thousands of partials, few outputs): one block per
-// output, fixed strided split + fixed shared-memory tree.  All deterministic.
+// Split-K jobs: 32 outputs per block, the partials split over its 8 warps, fixed-order
+// combine.  Column-sum jobs (thousands of partials, few outputs): one block per output,
+// fixed strided split + fixed shared-memory tree.  All deterministic.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ FinArgs a) {
   pdl_wait();
   const FinJob& j = a.job[blockIdx.y];
@@ -422,9 +426,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
   for (long long base = (long long)blockIdx.x * 32; base < total; base += (long long)gridDim.x * 32) {
     const long long i = base + lane;
     float s = 0.f;
+    // 32-bit index math (outputs < 2^31; a 64-bit division is a long software sequence)
+    const uint32_t iu = (uint32_t)i, mu = iu / (uint32_t)j.N, nu = iu - mu * (uint32_t)j.N;
     if (i < total) {
-      const long long m = i / j.N, n = i % j.N;
-      const float* p = j.partial + m * j.Npad + n;
+      const float* p = j.partial + (long long)mu * j.Npad + nu;
       for (int r = warp; r < j.splits; r += 64) {
         float v[8];
 #pragma unroll
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ F
       float t = red8[0][lane];
 #pragma unroll
       for (int w = 1; w < 8; ++w) t += red8[w][lane];
-      fin_store(a, j, i, t);
+      fin_store_mn(a, j, (int)mu, (int)nu, t);
     }
     __syncthreads();
   }
