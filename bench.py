@@ -380,7 +380,7 @@ def main():
 
     def e2e_measure(make):
         src = [make(T, B, A, dev, seed=200 + 7 * i + rank) for i in range(2)]
-        infeed = DeviceInfeed(src[0], dev)
+        infeed = DeviceInfeed(src[0], dev, depth=int(os.environ.get("BP_INFEED_DEPTH", "2")))
         host = []
         for b in src:  # pinned host rollouts in the infeed's packed layout (one H2D per step)
             h = infeed.alloc_host()
@@ -389,17 +389,19 @@ def main():
             host.append(h)
 
         def e2e_run(nsteps):
-            infeed.put(host[0])
+            ahead = min(infeed.depth - 1, nsteps)  # batches in flight on the copy stream
+            for j in range(ahead):
+                infeed.put(host[j % 2])
             out = None
             for i in range(nsteps):
                 b = infeed.get()
-                if i + 1 < nsteps:
-                    infeed.put(host[(i + 1) % 2])
+                if i + ahead < nsteps:
+                    infeed.put(host[(i + ahead) % 2])
                 out = learner.learn(FLAGS, None, model, b, (), opt, None, process_group=pg)
                 # (the next get() releases this slot on the stream: one native call per step)
             return out
 
-        e2e_run(6)  # per infeed slot: eager step, graph capture, replay -> timed steps replay only
+        e2e_run(3 * infeed.depth)  # per infeed slot: eager step, graph capture, replay -> timed steps replay only
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
