@@ -38,6 +38,13 @@ extern "C" {
 #define BP_STATUS_NEG_DISCOUNT 4u   /* discount < 0                -> SchemaError  (vtrace.py:109-110) */
 #define BP_STATUS_NONFINITE_LOSS 8u /* non-finite total loss       -> NonFiniteError (vtrace.py:202-205) */
 #define BP_STATUS_NONFINITE_GRAD 16u/* non-finite gradient         -> NonFiniteError (model.py:251-252) */
+#define BP_STATUS_BATCH_NONFINITE 32u /* learner loss only: NaN/inf in a batch field (reward,
+                                         behaviour logits) -> SchemaError in the learner step
+                                         (validate_batch, rollout.py:189-192), NonFiniteError in
+                                         compute_losses (vtrace.py:83-91) */
+/* Learner loss (bp_learner_loss_f32): any violation in the batch also makes the total loss NaN,
+ * so bp_rmsprop_clip_f32(reject_if_nonfinite = &losses[3]) rejects the step on every
+ * data-parallel rank after the loss all-reduce. */
 
 int bp_abi_version(void);
 const char* bp_last_error(void);
@@ -94,7 +101,8 @@ int bp_vtrace_from_importance_weights_f32(const float* log_rhos, const float* di
  * Outputs
  *   d_logits  : (T, B, A) f32   d total / d learner_logits
  *   d_baseline: (T+1, B) f32    d total / d learner_baseline, row T = 0
- *   vs, pg_advantages: (T, B) f32, nullable
+ *   vs, pg_advantages, clipped_rhos: (T, B) f32, nullable (clipped_rhos = min(rho_bar, rho),
+ *               VtraceResult.clipped_rhos vtrace.py:128)
  *   losses    : 4 doubles on device: pg, baseline(0.5*sum sq), entropy(-sum H), total
  *   workspace : bp_learner_loss_workspace_bytes(T, B, A) bytes, zeroed ONCE by
  *               the caller before first use (the kernel leaves it zeroed). */
@@ -105,7 +113,8 @@ int bp_learner_loss_f32(const float* learner_logits, const float* learner_baseli
                         float discount, float clip_rho, float clip_pg_rho, float clip_c,
                         float pg_cost, float baseline_cost, float entropy_cost, int reward_clip,
                         float* d_logits, float* d_baseline, float* vs, float* pg_advantages,
-                        double* losses, void* workspace, unsigned* status, void* stream);
+                        float* clipped_rhos, double* losses, void* workspace, unsigned* status,
+                        void* stream);
 
 /* ---------------------------------------------------------------------------
  * Optimiser: global-norm clip + RMSProp (eps outside the root, no momentum)
@@ -124,7 +133,8 @@ int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* workspace, void
  *   clip_mode 1: torch clip_grad_norm_ -- scale = min(1, max_norm/(norm + 1e-6))
  *   clip_mode 2: no clipping
  * The norm is read from *sumsq on the device (no host sync); a non-finite
- * norm rejects the whole step (params untouched, BP_STATUS_NONFINITE_GRAD).
+ * norm rejects the whole step (params untouched, BP_STATUS_NONFINITE_GRAD); so does a
+ * non-finite *reject_if_nonfinite (nullable: the step's f64 total loss).
  * square_avg and params are updated in place; grads are overwritten with the
  * clipped gradients when write_clipped_grads != 0 (torch semantics).
  * norm_out (nullable, device f32) receives the pre-clip norm.  lr is read
@@ -134,7 +144,33 @@ int bp_sumsq_f32(const float* x, int64_t n, double* sumsq, void* workspace, void
 int bp_rmsprop_clip_f32(float* params, float* grads, float* square_avg, int64_t n,
                         const double* sumsq, float max_norm, int clip_mode, float lr,
                         const float* lr_dev, float alpha, float eps, int write_clipped_grads,
-                        float* norm_out, void* bf16_mirror, unsigned* status, void* stream);
+                        float* norm_out, void* bf16_mirror, unsigned* status,
+                        const double* reject_if_nonfinite, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Loss helpers (north-star: upstream monobeast compute_policy_gradient_loss /
+ * compute_baseline_loss / compute_entropy_loss, sum-reduced; in-tree arithmetic
+ * beastpipe losses_from_targets vtrace.py:169-221).  Forward: one HBM pass, the f32 loss
+ * into *out (and the f64 sum into *out64, nullable), deterministic fixed-order reduction;
+ * workspace: bp_loss_workspace_bytes() zeroed bytes, one per concurrently running call.
+ * Backward: grad_out is the device f32 upstream gradient of the scalar loss; the result
+ * overwrites d_logits [rows][A] / d_advantages [n].
+ * pg: logits [rows][A] f32, actions [rows] int64 (out of range -> BP_STATUS_ACTION_RANGE,
+ * treated as action 0), advantages [rows] f32 (no gradient, upstream detaches them).
+ * ------------------------------------------------------------------------- */
+size_t bp_loss_workspace_bytes(void);
+int bp_pg_loss_f32(const float* logits, const int64_t* actions, const float* advantages, long long rows,
+                   int A, float* out, double* out64, void* workspace, unsigned* status, void* stream);
+int bp_baseline_loss_f32(const float* advantages, long long n, float* out, double* out64, void* workspace,
+                         void* stream);
+int bp_entropy_loss_f32(const float* logits, long long rows, int A, float* out, double* out64,
+                        void* workspace, unsigned* status, void* stream);
+int bp_pg_loss_bwd_f32(const float* logits, const int64_t* actions, const float* advantages, long long rows,
+                       int A, const float* grad_out, float* d_logits, void* stream);
+int bp_baseline_loss_bwd_f32(const float* advantages, long long n, const float* grad_out, float* d_advantages,
+                             void* stream);
+int bp_entropy_loss_bwd_f32(const float* logits, long long rows, int A, const float* grad_out,
+                            float* d_logits, void* stream);
 
 /* ---------------------------------------------------------------------------
  * AtariNet (north-star network; replaces the reference network seam
@@ -239,8 +275,12 @@ int bp_atari_backward_frames(const BpAtariNet* net, int n, const uint8_t* frames
  * LSTM core (AtariNet(use_lstm=True): upstream nn.LSTM(H, H, 2), H = 513 + A,
  * stepped per time row with the done reset core_state = notdone_t * core_state).
  * Input projections and weight / input gradients are tcgen05 GEMMs over all
- * N = T1*B rows; the recurrence runs as persistent cooperative kernels (one grid
- * barrier per step, W_hh resident in shared memory, f32 recurrent arithmetic).
+ * N = T1*B rows.  The recurrence (default) runs on 16-CTA thread-block clusters, one
+ * per 8 batch columns: each CTA holds its W_hh slice in registers as bf16 mma.sync
+ * fragments and exchanges h / partial W_hh^T dz over DSMEM on mbarriers (bf16 W_hh,
+ * h_{t-1} and dz operands, f32 accumulation and cell math).  The fallback
+ * (bp_lstm_set_mode(1), or no 16-CTA clusters) is a pair of grid-cooperative kernels
+ * with one grid barrier per step and W_hh resident in shared memory in f32.
  * G4 = 4H rounded up to a multiple of 128.  Buffers marked "zeroed once" must be
  * zero at allocation (padding columns are never written).
  * ------------------------------------------------------------------------- */
@@ -267,6 +307,9 @@ size_t bp_lstm_partial_floats(int hidden);
  * DSMEM exchange when available, else the grid-cooperative kernels), 1 cooperative,
  * 2 cluster.  Process-wide; for tests and diagnostics. */
 int bp_lstm_set_mode(int mode);
+/* 1 if the LSTM recurrence currently runs on the cluster kernels (bf16 recurrent operands),
+ * 0 if on the cooperative f32 kernels. */
+int bp_lstm_cluster_active(void);
 /* Diagnostics: per-step %globaltimer trace of CTA 0 of the recurrent kernels into
  * buf (device u64 [2][T1][4] + 2: forward phases, backward phases, forward start /
  * end of set-up); NULL disables. */
@@ -307,11 +350,12 @@ int bp_infeed_put(void* dst, const void* src, size_t bytes, void* stream, void* 
 int bp_infeed_get(void* stream, void* release_event, void* ready_event);
 /* Learner-step stats read-back (monobeast learn() stats: losses + episode returns of the
  * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
- * (nullable) into out = [32 B losses | tb B done | tb * 4 B returns] in one launch.  out may
- * be device memory or pinned host memory (written through its unified-address mapping: the
- * step's result reaches the host without a separate copy). */
+ * (nullable) and the status word (nullable; read, then cleared for the next step) into
+ * out = [32 B losses | 4 B status | 4 B pad | tb B done | tb * 4 B returns] in one launch.
+ * out may be device memory or pinned host memory (written through its unified-address
+ * mapping: the step's result reaches the host without a separate copy). */
 int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                  void* out, void* stream);
+                  unsigned* status, void* out, void* stream);
 /* Shifted-tap GEMM test entry (the convolution form of the engine):
  * C[m][n] = sum_t sum_c A[m + offs[t]][c] * B[n][t*Cin + c]; window_mode 0 = one TMA box
  * per tap, 1 / 2 = one shared window per channel block (descriptor base offset 0 / row&7).

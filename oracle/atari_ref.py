@@ -78,6 +78,169 @@ class AtariNetRef(nn.Module):
                      baseline=baseline.view(T, B), action=action.view(T, B)), core_state)
 
 
+# ---------------------------------------------------------------------------------------------
+# bf16-operand emulation of the GPU network (parity oracle for the tcgen05 kernels)
+#
+# The kernels (paper_1910_03552_b200/csrc/network.cu) round to bf16 at fixed storage points and
+# accumulate in f32.  Restating those roundings on top of the fp32 upstream graph turns the
+# comparison from "bf16 vs fp32" (ReLU sign flips of near-zero pre-activations dominate, ~10%
+# torso gradient noise) into "f32 vs f64 accumulation order" (~1e-6), so gradients can be pinned
+# tightly.  Storage points restated here (network.cu torso_forward / heads_backward /
+# torso_backward, lstm_cluster.cu):
+#   forward   every GEMM operand: weights (flat bf16 mirror), activations X1, X2, X3, core
+#             (relu(fc) | clip(r) | onehot(a) | 1), heads operand [W | b] (so the head BIASES are
+#             bf16 too); LSTM: [W_ih | b_ih + b_hh] (one bf16 bias), layer outputs, and in the
+#             cluster recurrence W_hh and h_{t-1}
+#   backward  G = [d_logits | d_baseline] bf16 (heads weight / bias / data gradients); every
+#             conv data gradient d_pre1/2/3 (= the gradient at the pre-activation, also the
+#             operand of the weight gradient and the summand of the bias gradient); d_fc for
+#             Wfc and X3 (but d bfc is the epilogue's f32 column sum); LSTM gate gradients
+#             dgates (all LSTM weight / input gradients and, cluster mode, the recurrent dz)
+# Not emulated: the cluster recurrence's MUFU tanh (~2^-11 relative).
+# ---------------------------------------------------------------------------------------------
+
+
+def bf16_round(t):
+    return t.to(torch.bfloat16).to(t.dtype)
+
+
+def st_bf16(t):
+    """Straight-through bf16 rounding: rounded forward, identity gradient."""
+    return t + (bf16_round(t) - t).detach()
+
+
+class _RoundGrad(torch.autograd.Function):
+    """Identity forward; the incoming gradient is rounded to bf16 (a bf16-stored dY)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return bf16_round(g)
+
+
+def rg_bf16(t):
+    return _RoundGrad.apply(t)
+
+
+def _relu(z, zabs, mask, band, stats, name):
+    """ReLU whose decision adopts the kernel's mask ONLY inside the accumulation-ambiguity band
+    |z| <= band * sum|terms| (the tensor cores' accumulation error, ~1e-5 relative to sum|terms|,
+    can legitimately flip the sign there); everywhere else the oracle's own sign decides, and
+    `stats[name]` counts kernel masks that disagree OUTSIDE the band (must be 0) and adoptions."""
+    own = z > 0
+    if mask is None:
+        return z * own.to(z.dtype)
+    mask = mask.to(own.device)
+    amb = z.abs() <= band * zabs
+    if stats is not None:
+        stats[name] = dict(disagree=int(((mask != own) & ~amb).sum()),
+                           adopted=int(((mask != own) & amb).sum()), total=int(z.numel()))
+    return z * torch.where(amb, mask, own).to(z.dtype)
+
+
+def emulated_core_input(model, inputs, masks=None, band=1e-4, mask_stats=None):
+    """The GPU `core` buffer (n, 513+A): [relu(fc) | clip(r) | onehot(last_a)], bf16 values,
+    with the kernels' storage roundings (see the block comment above).
+    masks: optional kernel ReLU decisions (conv1 (n,32,20,20), conv2 (n,64,9,9), conv3
+    (n,64,7,7), fc (n,512) bool), adopted only inside the ambiguity band (_relu)."""
+    x = inputs["frame"]
+    T, B = x.shape[:2]
+    n = T * B
+    dt = model.conv1.weight.dtype
+    x = torch.flatten(x, 0, 1).to(dt)  # u8 values are exact in bf16; the 1/255 is the epilogue's alpha
+    w = st_bf16
+    m = masks or (None,) * 4
+
+    def sab(fn, xin, wt, b):  # sum |terms| of a pre-activation (ambiguity-band scale)
+        if masks is None:
+            return None
+        with torch.no_grad():
+            return fn(xin.abs(), wt.abs()) + b.abs()
+
+    conv1 = lambda xx, ww: F.conv2d(xx, ww, None, stride=4) * (1.0 / 255.0)  # noqa: E731
+    z1 = rg_bf16(conv1(x, w(model.conv1.weight)) + model.conv1.bias[:, None, None])
+    a1 = st_bf16(_relu(z1, sab(conv1, x, w(model.conv1.weight), model.conv1.bias[:, None, None]), m[0], band,
+                       mask_stats, "conv1"))
+    conv2 = lambda xx, ww: F.conv2d(xx, ww, None, stride=2)  # noqa: E731
+    z2 = rg_bf16(conv2(a1, w(model.conv2.weight)) + model.conv2.bias[:, None, None])
+    a2 = st_bf16(_relu(z2, sab(conv2, a1, w(model.conv2.weight), model.conv2.bias[:, None, None]), m[1], band,
+                       mask_stats, "conv2"))
+    conv3 = lambda xx, ww: F.conv2d(xx, ww, None)  # noqa: E731
+    z3 = rg_bf16(conv3(a2, w(model.conv3.weight)) + model.conv3.bias[:, None, None])
+    a3 = st_bf16(_relu(z3, sab(conv3, a2, w(model.conv3.weight), model.conv3.bias[:, None, None]), m[2], band,
+                       mask_stats, "conv3"))
+    fc = lambda xx, ww: xx @ ww.t()  # noqa: E731
+    x3 = a3.reshape(n, -1)
+    zf = rg_bf16(fc(x3, w(model.fc.weight))) + model.fc.bias  # d bfc: f32 column sum
+    h = st_bf16(_relu(zf, sab(fc, x3, w(model.fc.weight), model.fc.bias), m[3], band, mask_stats, "fc"))
+    one_hot = F.one_hot(inputs["last_action"].reshape(n), model.num_actions).to(dt)
+    clipped_reward = st_bf16(torch.clamp(inputs["reward"], -1, 1).reshape(n, 1).to(dt))
+    return torch.cat([h, clipped_reward, one_hot], dim=-1)
+
+
+def emulated_lstm(model, core_input, done, core_state, recurrence_bf16=True):
+    """Upstream 2-layer nn.LSTM stepped with done resets, with the GPU's roundings.
+    core_input (T1*B, H); done (T1, B) bool; core_state (h, c) each (2, B, H).
+    recurrence_bf16: the cluster recurrence (bf16 W_hh, h_{t-1} and dz mma.sync operands);
+    False: the cooperative f32 recurrence (only the GEMM operands are bf16).
+    Returns (layer outputs [(T1, B, H)] * 2, (h_N, c_N))."""
+    T1, B = done.shape
+    H = core_input.shape[-1]
+    dt = core_input.dtype
+    inp = core_input.reshape(T1, B, H)
+    outs, hs, cs = [], [], []
+    for layer in range(2):
+        wih = getattr(model.core, f"weight_ih_l{layer}")
+        whh = getattr(model.core, f"weight_hh_l{layer}")
+        bias = getattr(model.core, f"bias_ih_l{layer}") + getattr(model.core, f"bias_hh_l{layer}")
+        gx = inp @ st_bf16(wih).t() + st_bf16(bias)
+        whh_op = st_bf16(whh) if recurrence_bf16 else whh
+        h, c = core_state[0][layer].to(dt), core_state[1][layer].to(dt)
+        seq = []
+        for t in range(T1):
+            nd = (~done[t]).to(dt)[:, None]
+            h, c = h * nd, c * nd
+            if recurrence_bf16:
+                z = rg_bf16(gx[t] + st_bf16(h) @ whh_op.t())
+            else:  # f32 recurrence; the weight-gradient GEMMs still see bf16 dgates / h_{t-1}
+                z = rg_bf16(gx[t]) + h @ whh.t()
+            i, f, g, o = z.chunk(4, -1)
+            c = torch.sigmoid(f) * c + torch.sigmoid(i) * torch.tanh(g)
+            h = torch.sigmoid(o) * torch.tanh(c)
+            seq.append(h)
+        out = torch.stack(seq)
+        outs.append(out)
+        hs.append(h)
+        cs.append(c)
+        inp = st_bf16(out)  # the next layer / the heads read the bf16 output sequence
+    return outs, (torch.stack(hs), torch.stack(cs))
+
+
+def emulated_forward(model, inputs, core_state=(), recurrence_bf16=True, masks=None, band=1e-4,
+                     mask_stats=None):
+    """AtariNetRef.forward restated with the GPU kernels' bf16 storage points; same outputs.
+    Run it on an fp64 copy of the model (any device) so the remaining difference to the
+    kernels is their accumulation (the tensor cores' f32 accumulation truncates: ~1e-5 of
+    sum|terms| at K = 3136, measured by tools/parity_diag.py).  masks / band / mask_stats: see
+    emulated_core_input and _relu."""
+    T, B = inputs["frame"].shape[:2]
+    n = T * B
+    core = emulated_core_input(model, inputs, masks, band, mask_stats)
+    state = tuple()
+    if model.use_lstm:
+        outs, state = emulated_lstm(model, core, inputs["done"], core_state, recurrence_bf16)
+        core = outs[1].reshape(n, -1)
+    core = st_bf16(core)
+    logits = rg_bf16(core @ st_bf16(model.policy.weight).t() + st_bf16(model.policy.bias))
+    baseline = rg_bf16(core @ st_bf16(model.baseline.weight).t() + st_bf16(model.baseline.bias))
+    action = torch.argmax(logits, dim=1)
+    return (dict(policy_logits=logits.view(T, B, model.num_actions), baseline=baseline.view(T, B),
+                 action=action.view(T, B)), state)
+
+
 def vtrace_from_logits(behavior_policy_logits, target_policy_logits, actions, discounts, rewards,
                        values, bootstrap_value, clip_rho_threshold=1.0, clip_pg_rho_threshold=1.0):
     """Upstream vtrace.from_logits (torch restatement; targets under no_grad)."""
@@ -106,9 +269,12 @@ def vtrace_from_logits(behavior_policy_logits, target_policy_logits, actions, di
     return vs, pg_adv
 
 
-def learn_losses(model, batch, flags, core_state=()):
-    """Upstream learn() up to total_loss (no optimiser); returns (total, parts, outputs)."""
-    out, _ = model(batch, core_state)
+def learn_losses(model, batch, flags, core_state=(), forward=None, scales=None):
+    """Upstream learn() up to total_loss (no optimiser); returns (total, parts, outputs).
+    forward: the network forward (default `model(batch, core_state)`; emulated_forward for the
+    bf16-operand oracle).  scales: an optional dict that receives sum|term| of each loss (the
+    tolerance basis for loss sums with cancellation)."""
+    out, _ = (forward or model)(batch, core_state)
     bootstrap_value = out["baseline"][-1]
     b = {k: v[1:] for k, v in batch.items()}
     o = {k: v[:-1] for k, v in out.items()}
@@ -124,7 +290,40 @@ def learn_losses(model, batch, flags, core_state=()):
     pol = F.softmax(o["policy_logits"], dim=-1)
     entropy_loss = flags["entropy_cost"] * torch.sum(pol * F.log_softmax(o["policy_logits"], dim=-1))
     total = pg_loss + baseline_loss + entropy_loss
+    if scales is not None:
+        with torch.no_grad():
+            scales["pg_loss"] = float(torch.sum(torch.abs(ce * pg_adv)))
+            scales["baseline_loss"] = float(baseline_loss)
+            scales["entropy_loss"] = float(torch.abs(entropy_loss))
+            scales["total_loss"] = scales["pg_loss"] + scales["baseline_loss"] + scales["entropy_loss"]
     return total, (pg_loss, baseline_loss, entropy_loss), out
+
+
+def learn_grads(model, batch, flags, core_state=(), forward=None):
+    """Upstream learn() up to the pre-optimiser gradients: (grads {name: tensor}, parts, scales).
+    With forward=emulated_forward (on an fp64 model) this is the bf16-operand parity oracle of
+    the fused learner step's flat gradients."""
+    scales = {}
+    total, parts, _ = learn_losses(model, batch, flags, core_state, forward=forward, scales=scales)
+    for p in model.parameters():
+        p.grad = None
+    total.backward()
+    grads = {k: p.grad.detach().clone() for k, p in model.named_parameters()}
+    return grads, dict(total_loss=float(total.detach()), pg_loss=float(parts[0].detach()),
+                       baseline_loss=float(parts[1].detach()), entropy_loss=float(parts[2].detach())), scales
+
+
+def rmsprop_first_update(grads, flags):
+    """clip_grad_norm_ (max/(norm+1e-6), clamped to 1) then the first torch RMSprop step from a
+    zero square_avg: the parameter update -lr g / (sqrt((1-alpha) g^2) + eps), per tensor."""
+    norm = torch.sqrt(sum(torch.sum(g.double() ** 2) for g in grads.values()))
+    coef = torch.clamp(flags["grad_norm_clipping"] / (norm + 1e-6), max=1.0)
+    out = {}
+    for k, g in grads.items():
+        g = g.double() * coef
+        sq = (1.0 - flags["alpha"]) * g * g
+        out[k] = -flags["learning_rate"] * g / (torch.sqrt(sq) + flags["epsilon"])
+    return out, float(norm)
 
 
 def learn_step(model, optimizer, batch, flags, core_state=()):

@@ -32,10 +32,17 @@ SIGNATURES: dict[str, tuple] = {
     "bp_vtrace_from_importance_weights_f32": (I, [P, P, P, P, P, I, I, F, F, F, P, P, P, P, P]),
     "bp_learner_loss_workspace_bytes": (SZ, [I, I, I]),
     "bp_learner_loss_f32": (I, [P, P, P, P, P, P, I, I, I, F, F, F, F, F, F, F, I,
-                                P, P, P, P, P, P, P, P]),
+                                P, P, P, P, P, P, P, P, P]),
     "bp_sumsq_workspace_bytes": (SZ, [I64]),
     "bp_sumsq_f32": (I, [P, I64, P, P, P]),
-    "bp_rmsprop_clip_f32": (I, [P, P, P, I64, P, F, I, F, P, F, F, I, P, P, P, P]),
+    "bp_rmsprop_clip_f32": (I, [P, P, P, I64, P, F, I, F, P, F, F, I, P, P, P, P, P]),
+    "bp_loss_workspace_bytes": (SZ, []),
+    "bp_pg_loss_f32": (I, [P, P, P, C.c_longlong, I, P, P, P, P, P]),
+    "bp_baseline_loss_f32": (I, [P, C.c_longlong, P, P, P, P]),
+    "bp_entropy_loss_f32": (I, [P, C.c_longlong, I, P, P, P, P, P]),
+    "bp_pg_loss_bwd_f32": (I, [P, P, P, C.c_longlong, I, P, P, P]),
+    "bp_baseline_loss_bwd_f32": (I, [P, C.c_longlong, P, P, P]),
+    "bp_entropy_loss_bwd_f32": (I, [P, C.c_longlong, I, P, P, P]),
     "bp_atari_param_count": (I64, [I, I]),
     "bp_atari_param_offsets": (I, [I, I, P]),
     "bp_atari_workspace_bytes": (SZ, [I, I]),
@@ -50,11 +57,12 @@ SIGNATURES: dict[str, tuple] = {
     "bp_lstm_partial_floats": (SZ, [I]),
     "bp_lstm_trace": (I, [P]),
     "bp_lstm_set_mode": (I, [I]),
+    "bp_lstm_cluster_active": (I, []),
     "bp_atari_lstm_forward": (I, [P, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_forward_planes": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
-    "bp_pack_stats": (I, [P, P, P, I, P, P]),
+    "bp_pack_stats": (I, [P, P, P, I, P, P, P]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),
     "bp_infeed_get": (I, [P, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),

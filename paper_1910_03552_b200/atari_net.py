@@ -126,17 +126,26 @@ class _Buffers:
         self.lstm = _LstmBuffers(num_actions, capacity, device) if use_lstm else None
 
 
+def _check_fwd_gen(ctx):
+    if ctx.net._fwd_gen != ctx.fwd_gen:
+        raise RuntimeError("AtariNet: backward after another forward on the same module; the fused "
+                           "kernels keep only the last forward's activations -- call backward "
+                           "before the next forward (or use a second AtariNet)")
+
+
 class _AtariFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, net, frames, reward, last_action, *params):
         logits, baseline = net._forward_kernels(frames, reward, last_action, repack=True)
         ctx.net = net
+        ctx.fwd_gen = net._fwd_gen
         ctx.save_for_backward(reward, last_action)
         return logits, baseline
 
     @staticmethod
     def backward(ctx, d_logits, d_baseline):
         net = ctx.net
+        _check_fwd_gen(ctx)
         reward, last_action = ctx.saved_tensors
         grads = torch.empty_like(net.flat_params)
         net._backward_kernels(d_logits, d_baseline, reward, last_action, grads)
@@ -150,6 +159,7 @@ class _AtariLstmFunction(torch.autograd.Function):
         lstm = dict(T1=T1, B=B, done=done, h0=h0, c0=c0)
         logits, baseline = net._forward_kernels(frames, reward, last_action, repack=True, lstm=lstm)
         ctx.net = net
+        ctx.fwd_gen = net._fwd_gen
         ctx.dims = (T1, B)
         ctx.save_for_backward(reward, last_action, done, c0)
         ctx.mark_non_differentiable(lstm["hN"], lstm["cN"])
@@ -158,6 +168,7 @@ class _AtariLstmFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, d_logits, d_baseline, d_hN, d_cN):
         net = ctx.net
+        _check_fwd_gen(ctx)
         reward, last_action, done, c0 = ctx.saved_tensors
         T1, B = ctx.dims
         grads = torch.empty_like(net.flat_params)
@@ -212,6 +223,12 @@ class AtariNet(nn.Module):
         self._register_state_dict_hook(AtariNet._to_torch_layout)
         self.register_load_state_dict_pre_hook(AtariNet._from_torch_layout)
         self._bufs: _Buffers | None = None
+        # bumped whenever the activation / workspace buffers are reallocated: CUDA graphs that
+        # captured the old addresses must be dropped (FusedLearner checks it)
+        self.buffer_generation = 0
+        # bumped by every forward: an autograd backward must follow ITS forward (the kernels
+        # read the activations the forward left in the shared buffers)
+        self._fwd_gen = 0
         self._logits = None
         self._baseline = None
         self.sample_seed = 0x5EED
@@ -252,6 +269,7 @@ class AtariNet(nn.Module):
             self._logits = torch.empty(n, self.num_actions, device=self.flat_params.device)
             self._baseline = torch.empty(n, device=self.flat_params.device)
             self.mirror_fresh = False
+            self.buffer_generation += 1
         return self._bufs
 
     @property
@@ -335,6 +353,7 @@ class AtariNet(nn.Module):
             else:
                 N.check(N.lib().bp_atari_forward(b.ref, n, N.ptr(frames), *tail), "bp_atari_forward")
         self._last_n = n
+        self._fwd_gen += 1
         # frame source of this forward, for the backward (kept alive until the next forward)
         self._frame_src = (frames, plane_index, num_planes if plane_index is not None else 0)
         return logits, baseline

@@ -1304,6 +1304,8 @@ static bool lstm_use_cluster() {
   return lstm_cluster_batch() > 0;
 }
 
+extern "C" int bp_lstm_cluster_active(void) { return lstm_use_cluster() ? 1 : 0; }
+
 static int lstm_g4(int H) { return (4 * H + 127) & ~127; }
 
 static int check_lstm(const BpAtariNet* net, const BpLstmCore* core, int T1, int B) {

@@ -98,13 +98,17 @@ __global__ void __launch_bounds__(kOptThreads)
                    const double* __restrict__ sumsq, float max_norm, int mode, float lr_host,
                    const float* __restrict__ lr_dev, float alpha, float eps, int write_grads,
                    float* __restrict__ norm_out, __nv_bfloat16* __restrict__ mirror,
-                   unsigned* status) {
+                   unsigned* status, const double* __restrict__ reject_loss) {
   pdl_wait();
-  const ClipScale cs = clip_scale(sumsq, max_norm, mode);
+  ClipScale cs = clip_scale(sumsq, max_norm, mode);
+  // the step's total loss is non-finite (a NaN loss, or a batch violation poisoned it):
+  // reject like a non-finite gradient, without a second status bit (the loss kernel set one)
+  const bool loss_ok = reject_loss == nullptr || isfinite(*reject_loss);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (norm_out) *norm_out = (float)sqrt(*sumsq);
-    if (!cs.ok) set_status(status, BP_STATUS_NONFINITE_GRAD);
+    if (!cs.ok && loss_ok) set_status(status, BP_STATUS_NONFINITE_GRAD);
   }
+  cs.ok = cs.ok && loss_ok;
   if (!cs.ok) return;  // reject the step, params untouched (model.py:251-252)
   const float lr = lr_dev ? *lr_dev : lr_host;
   const float sc = cs.scale;
@@ -149,19 +153,30 @@ __global__ void __launch_bounds__(kOptThreads)
   }
 }
 
-// stats read-back buffer: [losses 4 x f64 | done tb x u8 | returns tb x f32 at byte offset
-// 32 + tb (byte stores when that is not 4-byte aligned)]; one element per thread
+// stats read-back buffer: [losses 4 x f64 | status u32 | pad u32 | done tb x u8 | returns tb x f32
+// at byte offset 40 + tb (byte stores when that is not 4-byte aligned)]; one element per thread
+constexpr int kStatsHead = 40;
 __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restrict__ losses,
                                                          const uint8_t* __restrict__ done,
                                                          const float* __restrict__ ret, int tb,
+                                                         unsigned* __restrict__ status,
                                                          uint8_t* __restrict__ out) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 4) reinterpret_cast<double*>(out)[i] = losses[i];
+  if (i == 4) {  // the step's status word: read back, then cleared for the next step
+    unsigned st = 0u;
+    if (status) {
+      st = *status;
+      *status = 0u;
+    }
+    reinterpret_cast<unsigned*>(out)[8] = st;
+    reinterpret_cast<unsigned*>(out)[9] = 0u;
+  }
   if (i >= tb) return;
-  out[32 + i] = done[i] ? 1 : 0;
+  out[kStatsHead + i] = done[i] ? 1 : 0;
   if (ret) {
-    uint8_t* o = out + 32 + tb;
+    uint8_t* o = out + kStatsHead + tb;
     if ((tb & 3) == 0) {
       reinterpret_cast<float*>(o)[i] = ret[i];
     } else {
@@ -181,14 +196,14 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
 using namespace bp;
 
 extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                             void* out, void* stream) {
+                             unsigned* status, void* out, void* stream) {
   if (!losses || !done || !out || tb < 0) {
     set_error("pack_stats: bad args");
     return BP_ERR_ARG;
   }
-  const int n = tb > 4 ? tb : 4;
+  const int n = tb > 5 ? tb : 5;
   launch_pdl(pack_stats_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, losses, done,
-             episode_return, tb, reinterpret_cast<uint8_t*>(out));
+             episode_return, tb, status, reinterpret_cast<uint8_t*>(out));
   return check_launch("pack_stats_kernel");
 }
 
@@ -214,7 +229,7 @@ extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_av
                                    const double* sumsq, float max_norm, int clip_mode, float lr,
                                    const float* lr_dev, float alpha, float eps,
                                    int write_clipped_grads, float* norm_out, void* bf16_mirror,
-                                   unsigned* status, void* stream) {
+                                   unsigned* status, const double* reject_if_nonfinite, void* stream) {
   if (n < 0 || !params || !grads || !square_avg || !sumsq || clip_mode < 0 || clip_mode > 2) {
     set_error("rmsprop_clip: bad args");
     return BP_ERR_ARG;
@@ -223,6 +238,6 @@ extern "C" int bp_rmsprop_clip_f32(float* params, float* grads, float* square_av
   int grid = (int)(want < 1 ? 1 : (want > 8 * 148 ? 8 * 148 : want));
   launch_pdl(rmsprop_kernel, dim3(grid), dim3(kOptThreads), 0, (cudaStream_t)stream, params, grads, square_avg, n,
              sumsq, max_norm, clip_mode, lr, lr_dev, alpha, eps, write_clipped_grads, norm_out,
-             reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status);
+             reinterpret_cast<__nv_bfloat16*>(bf16_mirror), status, reject_if_nonfinite);
   return check_launch("rmsprop_kernel");
 }

@@ -36,8 +36,9 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
                const float* rew, const float* val, const float* boot, int T, int B, int A,
                float clip_rho, float clip_pg_rho, float clip_c, float discount, float pg_cost,
                float baseline_cost, float entropy_cost, int reward_clip, float* vs, float* pg,
-               float* log_rhos, float* beh_logp, float* tgt_logp, float* d_logits, float* d_baseline,
-               double* losses, void* workspace, size_t ws_bytes, unsigned* status, cudaStream_t s);
+               float* log_rhos, float* beh_logp, float* tgt_logp, float* clipped_rhos, float* d_logits,
+               float* d_baseline, double* losses, void* workspace, size_t ws_bytes, unsigned* status,
+               cudaStream_t s);
 
 
 enum { MODE_LOGITS = 0, MODE_IW = 1, MODE_LOSS = 2 };
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         const float blp = rb.xa - rb.lse;
         const float tlp = rt.xa - rt.lse;
         const float lr = tlp - blp;
+        const float raw_rv = rv;  // finiteness is checked before the clip (fminf drops a NaN)
         if constexpr (MODE == MODE_LOSS) {
           // discount = (float)gamma * ~done, exact (set in the prefetch above)
           if (g.reward_clip) {
@@ -356,8 +358,14 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
         } else {
           if (dv < 0.f) bad |= BP_STATUS_NEG_DISCOUNT;
         }
-        if (!(rb.finite && rt.finite && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(dv)))
+        if constexpr (MODE == MODE_LOSS) {
+          // learner step: a non-finite batch field (reward, behaviour logits) is a schema
+          // violation (validate_batch, rollout.py:189-192); the learner's own outputs are not
+          if (!(rb.finite && isfinite(raw_rv))) bad |= BP_STATUS_BATCH_NONFINITE;
+          if (!(rt.finite && isfinite(lr) && isfinite(vv) && isfinite(dv))) bad |= BP_STATUS_NONFINITE_IN;
+        } else if (!(rb.finite && rt.finite && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(dv))) {
           bad |= BP_STATUS_NONFINITE_IN;
+        }
         s_lr[si] = lr;
         if constexpr (MODE == MODE_LOSS) {
           s_lse[si] = rt.lse;
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
       s_delta[i] = cr * (s_rew[i] + dsc * vnext - s_val[i]);
       s_dc[i] = dsc * cc;
       s_lr[i] = fminf(g.clip_pg_rho, rho);
-      if constexpr (MODE == MODE_IW) {
+      if constexpr (MODE != MODE_LOGITS) {
         if (g.clipped_rhos) g.clipped_rhos[(size_t)t * B + b0 + b] = cr;
       }
     }
@@ -451,6 +459,9 @@ __global__ void __launch_bounds__(kThreads) vtrace_kernel(VtArgs g) {
     // ------------------------------------------------------- phase 3a: loss sums
     __shared__ double red[3][kThreads / 32];
     __shared__ bool is_last;
+    // any violation in this CTA poisons the loss sums: the total becomes NaN, which rejects
+    // the optimiser step on every data-parallel rank after the loss all-reduce
+    if (__syncthreads_or(bad != 0u) && tid == 0) pg_sum = __longlong_as_double(0x7ff8000000000000LL);
     pg_sum = warp_sum(pg_sum);
     base_sum = warp_sum(base_sum);
     ent_sum = warp_sum(ent_sum);
@@ -658,7 +669,7 @@ extern "C" int bp_vtrace_from_logits_f32(const float* behavior_logits, const flo
   const int rc = vt3_launch(false, behavior_logits, target_logits, actions, discounts, rewards, values,
                             bootstrap_value, T, B, A, clip_rho, clip_pg_rho, clip_c, 0.f, 0.f, 0.f, 0.f, 0,
                             vs, pg_advantages, log_rhos, behavior_logp, target_logp, nullptr, nullptr,
-                            nullptr, nullptr, 0, status, (cudaStream_t)stream);
+                            nullptr, nullptr, nullptr, 0, status, (cudaStream_t)stream);
   if (rc != BP_ERR_UNSUPPORTED) return rc;
   return launch_mode<MODE_LOGITS>(a, (cudaStream_t)stream,
                                   aligned16(behavior_logits) && aligned16(target_logits));
@@ -709,8 +720,8 @@ extern "C" int bp_learner_loss_f32(const float* learner_logits, const float* lea
                                    float discount, float clip_rho, float clip_pg_rho, float clip_c,
                                    float pg_cost, float baseline_cost, float entropy_cost,
                                    int reward_clip, float* d_logits, float* d_baseline, float* vs,
-                                   float* pg_advantages, double* losses, void* workspace,
-                                   unsigned* status, void* stream) {
+                                   float* pg_advantages, float* clipped_rhos, double* losses,
+                                   void* workspace, unsigned* status, void* stream) {
   if (int e = check_dims(T, B, A, true)) return e;
   if (!(clip_rho > 0.f && clip_pg_rho > 0.f && clip_c > 0.f) || !(discount > 0.f && discount <= 1.f)) {
     set_error("learner_loss: bad config (discount %g, clips %g %g %g)", discount, clip_rho,
@@ -742,6 +753,7 @@ extern "C" int bp_learner_loss_f32(const float* learner_logits, const float* lea
   a.reward_clip = reward_clip;
   a.vs = vs;
   a.pg = pg_advantages;
+  a.clipped_rhos = clipped_rhos;
   a.d_logits = d_logits;
   a.d_baseline = d_baseline;
   a.losses = losses;
@@ -752,7 +764,7 @@ extern "C" int bp_learner_loss_f32(const float* learner_logits, const float* lea
     int rc = vt3_launch(true, behavior_logits, learner_logits, actions, done, rewards, learner_baseline,
                         learner_baseline + (size_t)T * B, T, B, A, clip_rho, clip_pg_rho, clip_c,
                         discount, pg_cost, baseline_cost, entropy_cost, reward_clip, vs, pg_advantages,
-                        nullptr, nullptr, nullptr, d_logits, d_baseline, losses, workspace,
+                        nullptr, nullptr, nullptr, clipped_rhos, d_logits, d_baseline, losses, workspace,
                         bp_learner_loss_workspace_bytes(T, B, A), status, (cudaStream_t)stream);
     if (rc != BP_ERR_UNSUPPORTED) return rc;
   }

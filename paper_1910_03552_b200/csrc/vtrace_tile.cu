@@ -46,6 +46,7 @@ struct Args {
   float* log_rhos;
   float* beh_logp;
   float* tgt_logp;
+  float* clipped_rhos;  // MODE_LOSS (nullable)
   float* d_baseline;
   double* losses;
   double* partials;
@@ -291,6 +292,9 @@ __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args 
         const float rho = fast_exp(lr);
         const float cr = fminf(g.clip_rho, rho);
         pgr = fminf(g.clip_pg_rho, rho);
+        if constexpr (LOSS) {
+          if (g.clipped_rhos) g.clipped_rhos[idx] = cr;
+        }
         s_delta[tid] = cr * (rv + dv * vnext - vv);
         s_dc[tid] = dv * fminf(g.clip_c, rho);
         if constexpr (!LOSS) {
@@ -299,8 +303,15 @@ __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args 
           if (g.beh_logp) g.beh_logp[idx] = blp;
           if (g.tgt_logp) g.tgt_logp[idx] = tlp;
         }
-        if (!(fb && ft && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(vnext) && isfinite(dv)))
+        if constexpr (LOSS) {
+          // learner step: a non-finite batch field (reward, behaviour logits) is a schema
+          // violation (validate_batch, rollout.py:189-192); the learner's own outputs are not
+          if (!(fb && isfinite(cur.r))) bad |= BP_STATUS_BATCH_NONFINITE;  // (before the clip)
+          if (!(ft && isfinite(lr) && isfinite(vv) && isfinite(vnext) && isfinite(dv)))
+            bad |= BP_STATUS_NONFINITE_IN;
+        } else if (!(fb && ft && isfinite(lr) && isfinite(rv) && isfinite(vv) && isfinite(vnext) && isfinite(dv))) {
           bad |= BP_STATUS_NONFINITE_IN;
+        }
       }
       comp_sync(ncomp);
       // Warp-parallel reverse scan, one warp per column: acc_t = delta_t + (gamma_t c_t)
@@ -380,6 +391,9 @@ __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args 
     __shared__ double red[3][32];
     __shared__ bool is_last;
     const int lane = tid & 31, w = tid >> 5, nw = (blockDim.x + 31) >> 5;
+    // any violation in this CTA poisons the loss sums: the total becomes NaN, which rejects
+    // the optimiser step on every data-parallel rank after the loss all-reduce
+    if (__syncthreads_or(bad != 0u) && tid == 0) pg_sum = __longlong_as_double(0x7ff8000000000000LL);
     pg_sum = warp_sum(pg_sum);
     base_sum = warp_sum(base_sum);
     ent_sum = warp_sum(ent_sum);
@@ -453,8 +467,9 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
                const float* rew, const float* val, const float* boot, int T, int B, int A,
                float clip_rho, float clip_pg_rho, float clip_c, float discount, float pg_cost,
                float baseline_cost, float entropy_cost, int reward_clip, float* vs, float* pg,
-               float* log_rhos, float* beh_logp, float* tgt_logp, float* d_logits, float* d_baseline,
-               double* losses, void* workspace, size_t ws_bytes, unsigned* status, cudaStream_t s) {
+               float* log_rhos, float* beh_logp, float* tgt_logp, float* clipped_rhos, float* d_logits,
+               float* d_baseline, double* losses, void* workspace, size_t ws_bytes, unsigned* status,
+               cudaStream_t s) {
   using namespace vt3;
   static const int bt_env = [] {
     const char* e = std::getenv("BP_VT3_BT");
@@ -507,6 +522,7 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
   g.log_rhos = log_rhos;
   g.beh_logp = beh_logp;
   g.tgt_logp = tgt_logp;
+  g.clipped_rhos = clipped_rhos;
   g.d_baseline = d_baseline;
   g.losses = losses;
   g.status = status;

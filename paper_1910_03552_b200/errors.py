@@ -31,6 +31,7 @@ NONFINITE_IN = 2
 NEG_DISCOUNT = 4
 NONFINITE_LOSS = 8
 NONFINITE_GRAD = 16
+BATCH_NONFINITE = 32
 
 
 class StatusWord:
@@ -61,12 +62,19 @@ class StatusWord:
         raise_for_bits(bits, context)
 
 
-def raise_for_bits(bits: int, context: str = "") -> None:
+def raise_for_bits(bits: int, context: str = "", learner: bool = False) -> None:
+    """Raise the reference's exception for a status word.  learner=True maps a non-finite
+    batch field to SchemaError as the learner step's validate_batch does (rollout.py:189-192);
+    otherwise to NonFiniteError as _check_vtrace_inputs does (vtrace.py:83-91)."""
     where = f"{context}: " if context else ""
     if bits & ACTION_RANGE:
         raise SchemaError(f"{where}actions outside [0, num_actions)")
     if bits & NEG_DISCOUNT:
         raise SchemaError(f"{where}discounts must be non-negative")
+    if bits & BATCH_NONFINITE:
+        if learner:
+            raise SchemaError(f"{where}reward / policy_logits contain non-finite values")
+        raise NonFiniteError(f"{where}input contains non-finite values")
     if bits & NONFINITE_IN:
         raise NonFiniteError(f"{where}input contains non-finite values")
     if bits & NONFINITE_LOSS:

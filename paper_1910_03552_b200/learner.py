@@ -18,15 +18,27 @@ rewards / done, learner outputs rows [:-1], bootstrap = baseline[-1]).
 """
 from __future__ import annotations
 
+import collections
+import os
 import threading
 
 import numpy as np
 import torch
 
 from . import _native as N  # noqa: F401  (fail loudly if the library is missing)
-from .errors import SchemaError
+from .errors import NONFINITE_GRAD, NONFINITE_IN, NONFINITE_LOSS, SchemaError, StatusWord, raise_for_bits
 from .learner_ops import LearnerLoss, VtraceConfig
 from .optim import RMSprop, sumsq_
+
+# learner-input fields and their dtypes (upstream learn() batch; validate_batch rollout.py:160-192)
+_BATCH_DTYPES = {"reward": (torch.float32,), "done": (torch.bool,),
+                 "policy_logits": (torch.float32,), "action": (torch.int64,),
+                 "last_action": (torch.int64,), "frame": (torch.uint8,),
+                 "frame_planes": (torch.uint8,), "frame_index": (torch.int32,),
+                 "episode_return": (torch.float32,)}
+# max captured step graphs per learner (each pins its own memory pool); least recently used
+# graphs are evicted beyond this
+MAX_GRAPHS = int(os.environ.get("BP_MAX_GRAPHS", "4"))
 
 
 def _flag(flags, name, default=None):
@@ -60,16 +72,23 @@ class FusedLearner:
         self.losses = torch.zeros(4, dtype=torch.float64, device=dev)
         # stats read-back: losses + done[1:] + episode_return[1:], written by one kernel straight
         # into pinned (device-mapped) host memory: one device->host transfer per step, no copy node
-        self._stats_host = torch.empty(4 * 8 + unroll_length * batch_size * 5, dtype=torch.uint8,
+        self._stats_host = torch.empty(40 + unroll_length * batch_size * 5, dtype=torch.uint8,
                                        pin_memory=True)
         self._stats_event = torch.cuda.Event()
         # numpy views of the pinned read-back buffer (no per-step tensor/numpy conversions)
         tb = unroll_length * batch_size
         hnp = self._stats_host.numpy()
         self._np_losses = hnp[:32].view(np.float64)
-        self._np_done = hnp[32:32 + tb].view(np.bool_)
-        self._np_ret = hnp[32 + tb:].view(np.float32)
+        self._np_status = hnp[32:36].view(np.uint32)
+        self._np_done = hnp[40:40 + tb].view(np.bool_)
+        self._np_ret = hnp[40 + tb:].view(np.float32)
+        # this learner's device status word: the fused loss ORs violation bits into it, the
+        # optimiser rejects a step whose (all-reduced) total loss is non-finite, and the stats
+        # pack reads it back with the losses and clears it (include/beast_b200.h BP_STATUS_*)
+        self.status = StatusWord(dev)
         self.pg = process_group
+        # where a non-finite step dumps its batch (pipeline.py:254-268 _dump_batch)
+        self.logdir = _flag(flags, "logdir", None) or _flag(flags, "savedir", None)
         model.buffers_for(self.n)
         # LSTM core: the initial agent state is staged into fixed buffers (graph inputs)
         self.lstm = None
@@ -81,20 +100,60 @@ class FusedLearner:
         # CUDA graphs: one captured step per (batch buffer set, optimizer); see step()
         self.use_graphs = True
         self.kernels_per_step = 0
-        self._graphs: dict = {}
-        self._seen: set = set()
+        self._graphs: collections.OrderedDict = collections.OrderedDict()  # LRU, <= MAX_GRAPHS
+        self._seen: collections.OrderedDict = collections.OrderedDict()
+        self._validated: set = set()  # graph keys whose batch schema was checked
+        self._buf_gen = model.buffer_generation
 
     def _pg_is_nccl(self) -> bool:
         """NCCL collectives can be captured in a CUDA graph; gloo ones cannot."""
         grp = None if self.pg is True else self.pg
         return torch.distributed.get_backend(grp) == "nccl"
 
-    def _graph_key(self, batch, optimizer):
-        keys = (("frame_planes", "frame_index") if "frame_planes" in batch else ("frame",)) + (
+    def _fields(self, batch):
+        return (("frame_planes", "frame_index") if "frame_planes" in batch else ("frame",)) + (
             "reward", "done", "policy_logits", "action", "last_action")
+
+    def _graph_key(self, batch, optimizer):
+        """A captured step reads raw device addresses: key it on every batch tensor's address,
+        dtype, shape and strides, the optimiser, and the model's activation-buffer generation."""
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
-        return tuple(batch[k].data_ptr() for k in keys) + (
-            ep.data_ptr() if ep is not None else 0, id(optimizer))
+        ts = [batch[k] for k in self._fields(batch)] + ([ep] if ep is not None else [])
+        return tuple((t.data_ptr(), t.dtype, tuple(t.shape), t.stride()) for t in ts) + (
+            ep is not None, id(optimizer), self.model.buffer_generation)
+
+    def validate(self, batch):
+        """Host-side schema checks of validate_batch (rollout.py:160-192): shapes and dtypes
+        (done must be bool).  The data-dependent checks (action range, finite reward / logits)
+        run inside the fused loss kernel and are raised by stats()."""
+        T, B, A = self.T, self.B, self.model.num_actions
+        for k in self._fields(batch):
+            if k not in batch:
+                raise SchemaError(f"batch has no {k!r}")
+            v = batch[k]
+            if not isinstance(v, torch.Tensor) or not v.is_cuda:
+                raise SchemaError(f"{k}: expected a CUDA tensor")
+            if v.dtype not in _BATCH_DTYPES[k]:
+                raise SchemaError(f"{k}: dtype {v.dtype}, expected {_BATCH_DTYPES[k][0]}")
+            if not v.is_contiguous():
+                raise SchemaError(f"{k}: must be contiguous (time-major (T+1, B, ...))")
+        want = {"reward": (T + 1, B), "done": (T + 1, B), "action": (T + 1, B), "last_action": (T + 1, B),
+                "policy_logits": (T + 1, B, A)}
+        if "frame_planes" in batch:
+            want["frame_index"] = (T + 1, B, 4)
+        else:
+            want["frame"] = (T + 1, B) + tuple(self.model.observation_shape)
+        for k, shape in want.items():
+            if tuple(batch[k].shape) != shape:
+                raise SchemaError(f"{k}: dims {tuple(batch[k].shape)}, expected {shape}")
+        ep = batch.get("episode_return")
+        if ep is not None and tuple(ep.shape) != (T + 1, B):
+            raise SchemaError(f"episode_return: dims {tuple(ep.shape)}, expected ({T + 1}, {B})")
+
+    def _drop_graphs(self):
+        self._graphs.clear()
+        self._seen.clear()
+        self._validated.clear()
 
     def step(self, batch, optimizer=None, scheduler=None, initial_agent_state=()):
         """Enqueue one learner step on the current stream; returns the device loss vector.
@@ -113,12 +172,20 @@ class FusedLearner:
             else:
                 self.lstm["h0"].zero_()
                 self.lstm["c0"].zero_()
+        if self._buf_gen != self.model.buffer_generation:
+            # the model reallocated its activation buffers (e.g. a larger forward): every
+            # captured graph points at freed memory
+            self._drop_graphs()
+            self._buf_gen = self.model.buffer_generation
+        key = self._graph_key(batch, optimizer)
+        if key not in self._validated:
+            self.validate(batch)
+            self._validated.add(key)
         graphable = (self.use_graphs and (self.pg is None or self._pg_is_nccl()) and
                      (optimizer is None or (isinstance(optimizer, RMSprop) and
                                             optimizer.flat_params.data_ptr() ==
                                             self.model.flat_params.data_ptr())))
         if graphable:
-            key = self._graph_key(batch, optimizer)
             g = self._graphs.get(key)
             if g is None and key in self._seen:
                 optimizer and optimizer.sync_lr()
@@ -133,7 +200,10 @@ class FusedLearner:
                 self.kernels_per_step = int(N.lib().bp_launch_count() - c0)
                 torch.cuda.current_stream().wait_stream(side)
                 self._graphs[key] = g
+                while len(self._graphs) > MAX_GRAPHS:
+                    self._graphs.popitem(last=False)
             if g is not None:
+                self._graphs.move_to_end(key)
                 if optimizer is not None:
                     optimizer.sync_lr()
                 if self.model.mirror_stale():  # e.g. load_state_dict between steps
@@ -142,7 +212,9 @@ class FusedLearner:
                 if scheduler is not None:
                     scheduler.step()
                 return self.losses
-            self._seen.add(key)
+            self._seen[key] = True
+            while len(self._seen) > 4 * MAX_GRAPHS:
+                self._seen.popitem(last=False)
         self._step_eager(batch, optimizer)
         if scheduler is not None:
             scheduler.step()
@@ -177,7 +249,7 @@ class FusedLearner:
         self.loss(self.logits[:T * B].view(T, B, A), self.baseline.view(T + 1, B),
                   batch["policy_logits"][1:], batch["action"][1:], reward[1:], batch["done"][1:],
                   self.cfg, d_logits=self.d_logits[:T * B].view(T, B, A),
-                  d_baseline=self.d_baseline.view(T + 1, B), losses=self.losses)
+                  d_baseline=self.d_baseline.view(T + 1, B), losses=self.losses, status=self.status)
         # 3. backward into the flat gradient buffer
         m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
                             m.flat_grads, lstm=lstm)
@@ -188,13 +260,20 @@ class FusedLearner:
             grp = self.pg if self.pg is not True else None
             torch.distributed.all_reduce(m.flat_grads, op=torch.distributed.ReduceOp.SUM, group=grp)
             torch.distributed.all_reduce(self.losses, op=torch.distributed.ReduceOp.SUM, group=grp)
-        # 5. clip + RMSProp
+        # 5. clip + RMSProp.  A step whose (all-reduced) total loss is non-finite -- a NaN loss,
+        #    or a batch violation, which the loss kernel turns into a NaN total -- is rejected on
+        #    the device (model.py:251-252: parameters untouched); stats() then raises
         if optimizer is not None:
             if isinstance(optimizer, RMSprop) and optimizer.flat_params.data_ptr() == m.flat_params.data_ptr():
-                optimizer.step(max_norm=self.max_norm, mirror=m.flat_bf16)  # params + bf16 mirror
+                optimizer.step(max_norm=self.max_norm, mirror=m.flat_bf16,  # params + bf16 mirror
+                               status=self.status, reject_if_nonfinite=self.losses[3:])
                 m.mirror_fresh = True
                 m._packed_version = m.flat_params._version
-            else:  # any torch optimiser: device-side norm + clip, then its own step
+            else:  # any torch optimiser: check the step first (one sync), then clip + its own step
+                bits = self.status.bits()
+                if bits or not bool(torch.isfinite(self.losses[3])):
+                    self.status.clear()
+                    self._raise(batch, bits | NONFINITE_LOSS)
                 ss = torch.zeros(1, dtype=torch.float64, device=m.flat_grads.device)
                 sumsq_(m.flat_grads, ss)
                 coef = torch.clamp(self.max_norm / (ss.sqrt().float() + 1e-6), max=1.0)
@@ -220,7 +299,8 @@ class FusedLearner:
                 ep = ep.float().contiguous()
         losses = losses if losses.dtype == torch.float64 and losses.is_contiguous() else losses.double().contiguous()
         N.check(N.lib().bp_pack_stats(losses.data_ptr(), done.data_ptr(), ep.data_ptr() if ep is not None else None,
-                                      tb, host.data_ptr(), N.stream_handle(losses.device)), "bp_pack_stats")
+                                      tb, self.status.ptr(), host.data_ptr(), N.stream_handle(losses.device)),
+                "bp_pack_stats")
 
     def stats(self, batch, losses=None):
         """Upstream learn() stats dict from the step's packed read-back (one sync)."""
@@ -229,7 +309,11 @@ class FusedLearner:
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
         self._stats_event.record()
         self._stats_event.synchronize()
+        bits = int(self._np_status[0])
         pg, base, ent, total = self._np_losses.tolist()
+        if bits or not np.isfinite(total):
+            # a rank whose own batch is fine still sees its peers' violations as a NaN total
+            self._raise(batch, bits if bits else NONFINITE_LOSS)
         cfg = self.cfg
         returns = self._np_ret[self._np_done].tolist() if ep is not None else []
         return {
@@ -242,6 +326,31 @@ class FusedLearner:
             "baseline_loss": base * cfg.baseline_cost,
             "entropy_loss": ent * cfg.entropy_cost,
         }
+
+
+    def _raise(self, batch, bits):
+        """The reference's error contract for a learner step: batch schema violations raise
+        SchemaError (validate_batch, rollout.py:160-192); a non-finite loss or gradient dumps the
+        batch to <logdir>/diagnostic_batch.npz and raises NonFiniteError (pipeline.py:333-338,
+        vtrace.py:202-205, model.py:251-252).  The device already rejected the update."""
+        dumped = None
+        if bits & (NONFINITE_IN | NONFINITE_LOSS | NONFINITE_GRAD) and not bits & ~(
+                NONFINITE_IN | NONFINITE_LOSS | NONFINITE_GRAD) and self.logdir:
+            dumped = dump_batch(batch, self.logdir)
+        try:
+            raise_for_bits(bits, "learner step", learner=True)
+        except Exception as e:
+            if dumped:
+                e.add_note(f"offending batch dumped to {dumped}")
+            raise
+
+
+def dump_batch(batch, logdir) -> str:
+    """pipeline.py:254-268 `_dump_batch`: the offending learner batch as diagnostic_batch.npz."""
+    os.makedirs(logdir, exist_ok=True)
+    path = os.path.join(logdir, "diagnostic_batch.npz")
+    np.savez(path, **{k: v.detach().cpu().numpy() for k, v in batch.items() if isinstance(v, torch.Tensor)})
+    return path
 
 
 def learn(flags, actor_model, model, batch, initial_agent_state, optimizer, scheduler,
@@ -300,7 +409,7 @@ class DeviceInfeed:
         for ev in self.events + self.freed:
             ev.record(self.stream)
         self._stream_h = self.stream.cuda_stream
-        self._released = True
+        self.state = [self._FREE] * depth
         self.head = 0  # next slot to fill
         self.tail = 0  # next slot to consume
         self.bytes_per_batch = sum(v.numel() * v.element_size() for v in like.values())
@@ -320,46 +429,79 @@ class DeviceInfeed:
         views["__flat__"] = flat
         return views
 
-    def put(self, host_batch: dict) -> None:
+    # slot life cycle (host-side bookkeeping; the device ordering is by events):
+    #   free -> filled (put: H2D copy enqueued) -> consumed (get: the compute stream waits for
+    #   the copy; steps enqueued after get() read it) -> released (freed event recorded on the
+    #   compute stream after those steps) -> filled ...
+    _FREE, _FILLED, _CONSUMED, _RELEASED = range(4)
+
+    def _release_slot(self, slot: int) -> None:
+        self.freed[slot].record(torch.cuda.current_stream(self.device))
+        self.state[slot] = self._RELEASED
+
+    def _claim_for_put(self) -> tuple[int, bool]:
+        """The slot the next put() fills, and whether its copy must wait for a release.
+        Raises if the producer ran a full ring ahead of the consumer (the slot still holds a
+        batch nobody consumed).  A consumed slot that was never release()d is released HERE, on
+        the current stream: the steps that read it were enqueued before this put (get(); step;
+        put() order), so the copy cannot overwrite a batch an in-flight step still reads."""
         slot = self.head % self.depth
+        st = self.state[slot]
+        if st == self._FILLED:
+            raise RuntimeError("DeviceInfeed.put(): ring full -- every slot holds a batch that was "
+                               "not yet consumed by get()")
+        if st == self._CONSUMED:
+            self._release_slot(slot)
+        return slot, self.state[slot] == self._RELEASED
+
+    def put(self, host_batch: dict) -> None:
+        slot, wait = self._claim_for_put()
         flat = host_batch.get("__flat__")
         if flat is not None and flat.numel() == self.packed_bytes and flat.is_pinned():
             # packed pinned batch: wait-for-release + one H2D copy + ready event in one C call
             N.check(N.lib().bp_infeed_put(self.flat[slot].data_ptr(), flat.data_ptr(), self.packed_bytes,
-                                          self._stream_h,
-                                          self.freed[slot].cuda_event if self.head >= self.depth else None,
+                                          self._stream_h, self.freed[slot].cuda_event if wait else None,
                                           self.events[slot].cuda_event), "bp_infeed_put")
-            self.head += 1
-            return
-        with torch.cuda.stream(self.stream):
-            if self.head >= self.depth:
-                self.stream.wait_event(self.freed[slot])  # consumer done with this slot
-            flat = host_batch.get("__flat__")
-            if flat is not None and flat.numel() == self.packed_bytes:
-                self.flat[slot].copy_(flat, non_blocking=True)
-            else:
-                for k, v in host_batch.items():
-                    self.slots[slot][k].copy_(v, non_blocking=True)
-            self.events[slot].record(self.stream)
+        else:
+            with torch.cuda.stream(self.stream):
+                if wait:
+                    self.stream.wait_event(self.freed[slot])  # consumer done with this slot
+                if flat is not None and flat.numel() == self.packed_bytes:
+                    self.flat[slot].copy_(flat, non_blocking=True)
+                else:
+                    for k, v in host_batch.items():
+                        self.slots[slot][k].copy_(v, non_blocking=True)
+                self.events[slot].record(self.stream)
+        self.state[slot] = self._FILLED
         self.head += 1
 
     def get(self) -> dict:
-        """The next filled slot; the current stream waits for its copy.  A slot consumed
-        before and not yet release()d is released first (at this point of the stream)."""
+        """The next filled slot; the current stream waits for its copy.  Every other slot that
+        was consumed and not yet release()d is released first (at this point of the stream, i.e.
+        after the steps enqueued on it so far)."""
         if self.tail >= self.head:
             raise RuntimeError("DeviceInfeed.get() without a pending put()")
         slot = self.tail % self.depth
-        prev = (self.tail - 1) % self.depth
-        rel = self.freed[prev].cuda_event if self.tail > 0 and not self._released else None
-        N.check(N.lib().bp_infeed_get(torch.cuda.current_stream(self.device).cuda_stream, rel,
+        assert self.state[slot] == self._FILLED
+        rel = None
+        for other in range(self.depth):
+            if other != slot and self.state[other] == self._CONSUMED:
+                if rel is None:  # one release rides in the C call, any further ones here
+                    rel = other
+                else:
+                    self._release_slot(other)
+        N.check(N.lib().bp_infeed_get(torch.cuda.current_stream(self.device).cuda_stream,
+                                      self.freed[rel].cuda_event if rel is not None else None,
                                       self.events[slot].cuda_event), "bp_infeed_get")
+        if rel is not None:
+            self.state[rel] = self._RELEASED
+        self.state[slot] = self._CONSUMED
         self.tail += 1
-        self._released = False
         return self.slots[slot]
 
     def release(self) -> None:
-        """Mark the most recently consumed slot reusable (after its step was enqueued).
-        Optional: get() releases the previous slot itself."""
+        """Mark the most recently consumed slot reusable (after its step was enqueued on the
+        current stream).  Optional: get() and put() release consumed slots themselves."""
         slot = (self.tail - 1) % self.depth
-        self.freed[slot].record(torch.cuda.current_stream(self.device))
-        self._released = True
+        if self.tail > 0 and self.state[slot] == self._CONSUMED:
+            self._release_slot(slot)

@@ -142,7 +142,7 @@ class LearnerLoss:
 
     def __call__(self, learner_logits, learner_baseline, behavior_logits, actions, rewards, done,
                  cfg: VtraceConfig, d_logits=None, d_baseline=None, vs=None, pg_advantages=None,
-                 losses=None, status=None):
+                 losses=None, status=None, clipped_rhos=None):
         T, B, A = learner_logits.shape[-3], learner_logits.shape[-2], learner_logits.shape[-1]
         if d_logits is None:
             d_logits = torch.empty((T, B, A), dtype=torch.float32, device=self.device)
@@ -157,7 +157,7 @@ class LearnerLoss:
             N.ptr(rewards), N.ptr(done), T, B, A, float(cfg.discount), float(cfg.rho_bar),
             float(pg_bar), float(cfg.c_bar), float(cfg.pg_cost), float(cfg.baseline_cost),
             float(cfg.entropy_cost), int(bool(cfg.reward_clip)), N.ptr(d_logits),
-            N.ptr(d_baseline), N.ptr(vs), N.ptr(pg_advantages), N.ptr(losses),
+            N.ptr(d_baseline), N.ptr(vs), N.ptr(pg_advantages), N.ptr(clipped_rhos), N.ptr(losses),
             N.ptr(self.workspace(T, B, A)), sw.ptr(), N.stream_handle(self.device)),
             "bp_learner_loss_f32")
         return d_logits, d_baseline, losses
@@ -203,14 +203,14 @@ def compute_losses(batch, learner_logits, learner_baseline, cfg: VtraceConfig):
     act = act_rows[s:s + t_len]
     vs = torch.empty((t_len, b), device=dev)
     pg = torch.empty((t_len, b), device=dev)
+    cr = torch.empty((t_len, b), device=dev)
     ll = _launcher(dev)
     losses = torch.empty(4, dtype=torch.float64, device=dev)
     d_logits, d_baseline, losses = ll(lg, bl, beh, act, rew_rows[1:], done_rows[1:], cfg,
-                                      vs=vs, pg_advantages=pg, losses=losses)
+                                      vs=vs, pg_advantages=pg, losses=losses, clipped_rhos=cr)
     status_word(dev).check("compute_losses")
     lv = losses.cpu().tolist()
     bundle = LossBundle(pg_loss=lv[0], baseline_loss=lv[1], entropy_loss=lv[2], total=lv[3])
-    # clipped rhos are not materialised by the fused kernel; recompute lazily only on request
     targets = VtraceResult(vs=out_like(vs, as_np), pg_advantages=out_like(pg, as_np),
-                           clipped_rhos=None)
+                           clipped_rhos=out_like(cr, as_np))
     return bundle, out_like(d_logits, as_np), out_like(d_baseline, as_np), targets

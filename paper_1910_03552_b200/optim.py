@@ -50,14 +50,17 @@ def rmsprop_clip_(params: torch.Tensor, grads: torch.Tensor, square_avg: torch.T
                   sumsq: torch.Tensor, *, lr: float, alpha: float, eps: float, max_norm: float,
                   clip_mode: str = "torch", lr_dev: torch.Tensor | None = None,
                   write_clipped_grads: bool = True, norm_out: torch.Tensor | None = None,
-                  mirror: torch.Tensor | None = None, status=None) -> None:
-    """In-place clip + RMSProp over flat buffers, norm read from `sumsq` on device."""
+                  mirror: torch.Tensor | None = None, status=None,
+                  reject_if_nonfinite: torch.Tensor | None = None) -> None:
+    """In-place clip + RMSProp over flat buffers, norm read from `sumsq` on device.
+    reject_if_nonfinite: a device f64 scalar (the step's total loss); non-finite -> the
+    whole update is rejected on device, like a non-finite gradient norm."""
     sw = status if status is not None else status_word(params.device)
     N.check(N.lib().bp_rmsprop_clip_f32(
         N.ptr(params), N.ptr(grads), N.ptr(square_avg), params.numel(), N.ptr(sumsq),
         float(max_norm), CLIP_MODES[clip_mode], float(lr), N.ptr(lr_dev), float(alpha),
         float(eps), int(write_clipped_grads), N.ptr(norm_out), N.ptr(mirror), sw.ptr(),
-        N.stream_handle(params.device)), "bp_rmsprop_clip_f32")
+        N.ptr(reject_if_nonfinite), N.stream_handle(params.device)), "bp_rmsprop_clip_f32")
 
 
 def flatten_params_(params: list[torch.nn.Parameter], device) -> tuple[torch.Tensor, torch.Tensor]:
@@ -153,7 +156,11 @@ class RMSprop(torch.optim.Optimizer):
             self._lr_host = lr
 
     @torch.no_grad()
-    def step(self, closure=None, max_norm: float | None = None, mirror: torch.Tensor | None = None):
+    def step(self, closure=None, max_norm: float | None = None, mirror: torch.Tensor | None = None,
+             status=None, reject_if_nonfinite: torch.Tensor | None = None):
+        """One fused clip + RMSProp update.  status: the StatusWord that receives
+        BP_STATUS_NONFINITE_GRAD (default: the per-device word); reject_if_nonfinite: a device
+        f64 scalar (the learner step's total loss) whose non-finite value rejects the update."""
         loss = closure() if closure is not None else None
         if not torch.cuda.is_current_stream_capturing():
             self.sync_lr()
@@ -167,7 +174,8 @@ class RMSprop(torch.optim.Optimizer):
         rmsprop_clip_(self.flat_params, self.flat_grads, self.square_avg, self._sumsq,
                       lr=g["lr"], alpha=g["alpha"], eps=g["eps"],
                       max_norm=float(max_norm or 0.0), clip_mode=mode, lr_dev=self.lr_dev,
-                      norm_out=self.norm, mirror=mirror)
+                      norm_out=self.norm, mirror=mirror, status=status,
+                      reject_if_nonfinite=reject_if_nonfinite)
         return loss
 
 

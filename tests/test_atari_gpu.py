@@ -1,13 +1,14 @@
 """AtariNet on tcgen05 vs the torch-CPU fp32 oracle (oracle/atari_ref.py) with
 identical weights.  The network runs bf16 operands / f32 accumulation; stated
-bounds: logits / baseline relative L2 <= 1e-2; parameter gradients <= 2e-2
-when the oracle backward uses the GPU forward's ReLU masks (kernel
-correctness), and <= 0.2 (torso) / 2e-2 (heads) end-to-end, where bf16-vs-fp32
-ReLU sign flips of near-zero pre-activations dominate."""
+bounds: against the fp32 upstream graph, logits / baseline relative L2 <= 1e-2 and
+parameter gradients <= 2e-2 through the GPU's ReLU masks; against the bf16-emulating
+oracle (oracle/atari_ref.emulated_forward), logits / baseline <= 1e-3 and every
+parameter gradient <= 5e-3 end to end."""
 import numpy as np
 import pytest
 import torch
 
+from conftest import gpu_relu_masks, parity_log
 from oracle import atari_ref
 
 pytestmark = pytest.mark.gpu
@@ -42,17 +43,6 @@ def test_forward_matches_oracle(T, B, A):
         got, _ = net({k: v.cuda() for k, v in batch.items()})
     assert rel_l2(got["policy_logits"], want["policy_logits"]) < 1e-2
     assert rel_l2(got["baseline"], want["baseline"]) < 1e-2
-
-
-def _gpu_masks(net, n):
-    """ReLU masks of the GPU forward, in torch NCHW layout (from the bf16 activation buffers)."""
-    t = net._bufs.t
-    x1 = t["x1"][: n * 100].float().cpu().view(n, 10, 10, 2, 2, 32)
-    m1 = x1.permute(0, 5, 1, 3, 2, 4).reshape(n, 32, 20, 20) > 0
-    m2 = t["x2"][: n * 81].float().cpu().view(n, 9, 9, 64).permute(0, 3, 1, 2) > 0
-    m3 = t["x3"][:n].float().cpu().view(n, 7, 7, 64).permute(0, 3, 1, 2) > 0
-    mf = t["core"][:n, :512].float().cpu() > 0
-    return m1, m2, m3, mf
 
 
 def _oracle_grads(ref, batch, dl, db, masks=None):
@@ -97,31 +87,44 @@ def test_backward_matches_masked_oracle(T, B, A):
     dl = torch.randn(n, A, generator=g)
     db = torch.randn(n, generator=g)
     got = _gpu_grads(net, batch, dl, db)
-    want = _oracle_grads(ref, batch, dl, db, masks=_gpu_masks(net, n))
+    want = _oracle_grads(ref, batch, dl, db, masks=gpu_relu_masks(net, n))
     errs = {k: rel_l2(got[k], w) for k, w in want.items()}
     assert all(torch.isfinite(v).all() for v in got.values())
     assert max(errs.values()) < 2e-2, errs
 
 
 @pytest.mark.parametrize("T,B,A", [(7, 16, 18), (80, 32, 6)])
-def test_backward_end_to_end_vs_fp32_oracle(T, B, A):
-    """Unmasked: ReLU sign flips between the bf16 and fp32 forwards add noise that
-    grows toward the input layer (stated bound: heads 2e-2, torso 0.2 rel L2,
-    cosine >= 0.98)."""
+def test_forward_backward_match_bf16_emulating_oracle(T, B, A):
+    """End to end against oracle/atari_ref.emulated_forward (fp64, the kernels' bf16 storage
+    points restated; ReLU decisions adopted only inside the accumulation-ambiguity band):
+    logits / baseline relative L2 <= 1e-3, every parameter gradient <= 5e-3."""
+    import copy
+
     net, ref = _models(A, seed=3)
     batch = atari_ref.synthetic_batch(T, B, A, seed=2)
     n = (T + 1) * B
     g = torch.Generator().manual_seed(5)
     dl = torch.randn(n, A, generator=g)
     db = torch.randn(n, generator=g)
-    got = _gpu_grads(net, batch, dl, db)
-    want = _oracle_grads(ref, batch, dl, db)
-    for k, w in want.items():
-        e = rel_l2(got[k], w)
-        cos = float(torch.nn.functional.cosine_similarity(got[k].cpu().double().reshape(1, -1),
-                                                          w.double().reshape(1, -1)))
-        bound = 2e-2 if k.startswith(("policy", "baseline")) else 0.2
-        assert e < bound and cos > 0.98, (k, e, cos)
+    cb = {k: v.cuda() for k, v in batch.items()}
+    logits, base = net._forward_kernels(cb["frame"].reshape(n, 4, 84, 84), cb["reward"].reshape(n),
+                                        cb["last_action"].reshape(n))
+    logits, base = logits.clone(), base.clone()
+    grads = torch.full_like(net.flat_params, float("nan"))
+    net._backward_kernels(dl.cuda(), db.cuda(), cb["reward"].reshape(n), cb["last_action"].reshape(n), grads)
+    torch.cuda.synchronize()
+    got = net.torch_layout_grads(grads)
+    ref64 = copy.deepcopy(ref).double().cuda()
+    stats = {}
+    out, _ = atari_ref.emulated_forward(ref64, cb, masks=gpu_relu_masks(net, n), mask_stats=stats)
+    assert rel_l2(logits, out["policy_logits"].reshape(n, A)) < 1e-3
+    assert rel_l2(base, out["baseline"].reshape(n)) < 1e-3
+    torch.autograd.backward([out["policy_logits"].reshape(n, A), out["baseline"].reshape(n)],
+                            [dl.double().cuda(), db.double().cuda()])
+    errs = {k: rel_l2(got[k], p.grad) for k, p in ref64.named_parameters()}
+    parity_log(f"atari bwd T={T} B={B} A={A}", dict(grad_rel_l2=errs, masks=stats))
+    assert max(errs.values()) < 5e-3, errs
+    assert all(s["disagree"] <= 1e-6 * s["total"] for s in stats.values()), stats
 
 
 def test_autograd_path_matches_kernels():

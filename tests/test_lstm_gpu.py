@@ -9,14 +9,13 @@ recurrence, its bf16 mma.sync operands (W_hh, h_{t-1}, and dz in backward) and
 MUFU tanh (~2^-11); everything else is f32 on the GPU.  Both recurrence
 implementations (grid-cooperative f32, cluster/DSMEM) are tested.  Stated bounds: final state (h_N, c_N, f32) relative L2 <= 2e-4; the bf16
 layer outputs <= 4e-3; LSTM / heads parameter gradients (bf16 gate-gradient
-operands in the weight-gradient GEMMs) <= 2e-2.  End to end against the
-torch-CPU fp32 upstream restatement: logits / baseline <= 2e-2, and learn()'s
-first-step pg / baseline losses within 1e-2 (the total within 1e-2 of the sum of
-their magnitudes: they partly cancel), gradient norm within 5e-2, update cosine
->= 0.9."""
+operands in the weight-gradient GEMMs) <= 2e-2 (measured <= 2.2e-3).  End to end against
+the torch-CPU fp32 upstream restatement: logits / baseline <= 2e-2.  learn() with the LSTM
+core (T1 = 81) is pinned against the bf16-emulating oracle in test_learn_parity_gpu.py."""
 import pytest
 import torch
 
+from conftest import parity_log
 from oracle import atari_ref
 
 pytestmark = pytest.mark.gpu
@@ -26,14 +25,6 @@ def rel_l2(a, b):
     a = a.double().cpu()
     b = b.double().cpu()
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
-
-
-def _bf(t):
-    return t.to(torch.bfloat16).double()
-
-
-def _st(t):  # straight-through bf16 rounding (forward rounded, gradient identity)
-    return t + (_bf(t) - t).detach()
 
 
 def _models(A, seed=0):
@@ -74,51 +65,14 @@ def lstm_mode(request):
     N.lib().bp_lstm_set_mode(0)
 
 
-class _RoundGrad(torch.autograd.Function):
-    """Identity forward; bf16-rounded gradient backward (the cluster path's bf16 dz operand)."""
-
-    @staticmethod
-    def forward(ctx, x):
-        return x.view_as(x)
-
-    @staticmethod
-    def backward(ctx, g):
-        return _bf(g)
-
-
 def _lstm_ref(ref, x, done, state, H, whh_bf16=False):
-    """float64 2-layer LSTM with done resets on the GPU core input x (n, H); returns the
-    layer outputs (T1, B, H) x 2 and the final (h, c) (2, B, H), autograd-enabled.
-    whh_bf16: emulate the cluster path's recurrent MMA, whose operands W_hh, h_{t-1}
-    and (backward) the gate gradients dz are bf16."""
-    T1, B = done.shape
-    outs, hs, cs = [], [], []
-    inp = x.view(T1, B, H)
-    for l in range(2):
-        wih = getattr(ref.core, f"weight_ih_l{l}")
-        whh = getattr(ref.core, f"weight_hh_l{l}")
-        whh = _st(whh) if whh_bf16 else whh
-        bias = getattr(ref.core, f"bias_ih_l{l}") + getattr(ref.core, f"bias_hh_l{l}")
-        gx = inp @ _st(wih).t() + _st(bias)
-        h, c = state[0][l].double(), state[1][l].double()
-        seq = []
-        for t in range(T1):
-            nd = (~done[t]).double()[:, None]
-            h, c = h * nd, c * nd
-            if whh_bf16:
-                z = _RoundGrad.apply(gx[t] + _st(h) @ whh.t())
-            else:
-                z = gx[t] + h @ whh.t()
-            i, f, gg, o = z.chunk(4, -1)
-            c = torch.sigmoid(f) * c + torch.sigmoid(i) * torch.tanh(gg)
-            h = torch.sigmoid(o) * torch.tanh(c)
-            seq.append(h)
-        out = torch.stack(seq)
-        outs.append(out)
-        hs.append(h)
-        cs.append(c)
-        inp = _st(out)  # the layer-2 input is the bf16 output sequence
-    return outs, torch.stack(hs), torch.stack(cs)
+    """float64 2-layer LSTM with done resets on the GPU core input x (n, H) -- the oracle's
+    bf16-emulating restatement (oracle/atari_ref.emulated_lstm); returns the layer outputs
+    (T1, B, H) x 2 and the final (h, c) (2, B, H), autograd-enabled.  whh_bf16: emulate the
+    cluster path's recurrent MMA, whose operands W_hh, h_{t-1} and (backward) dz are bf16."""
+    outs, (hN, cN) = atari_ref.emulated_lstm(ref, x, done, tuple(s.double() for s in state),
+                                             recurrence_bf16=whh_bf16)
+    return outs, hN, cN
 
 
 def _run_gpu(net, batch, state, T1, B):
@@ -132,7 +86,7 @@ def _run_gpu(net, batch, state, T1, B):
     return cb, lstm, logits, baseline
 
 
-@pytest.mark.parametrize("T1,B,A", [(3, 2, 6), (9, 32, 18), (5, 40, 6), (4, 75, 31)])
+@pytest.mark.parametrize("T1,B,A", [(3, 2, 6), (9, 32, 18), (5, 40, 6), (4, 75, 31), (81, 32, 18)])
 def test_recurrence_matches_float64(T1, B, A, lstm_mode):
     net, ref = _models(A)
     ref = ref.double()
@@ -146,6 +100,9 @@ def test_recurrence_matches_float64(T1, B, A, lstm_mode):
     with torch.no_grad():
         outs, hN, cN = _lstm_ref(ref, x, batch["done"], state, H, whh_bf16=lstm_mode == 2)
     tol = 2e-4 if lstm_mode == 1 else 1e-3  # cluster: bf16 h_{t-1} rounding flips near ties
+    parity_log(f"lstm fwd T1={T1} B={B} A={A} mode={lstm_mode}",
+               dict(hN=rel_l2(lstm["hN"], hN), cN=rel_l2(lstm["cN"], cN),
+                    out=[rel_l2(L["out"][l, :n, :H].double().cpu().view(T1, B, H), outs[l]) for l in range(2)]))
     assert rel_l2(lstm["hN"], hN) < tol
     assert rel_l2(lstm["cN"], cN) < tol
     for l in range(2):
@@ -154,7 +111,7 @@ def test_recurrence_matches_float64(T1, B, A, lstm_mode):
         assert torch.all(L["out"][l, :n, H] == 1)  # bias column of the augmented rows
 
 
-@pytest.mark.parametrize("T1,B,A", [(4, 3, 6), (12, 32, 18)])
+@pytest.mark.parametrize("T1,B,A", [(4, 3, 6), (12, 32, 18), (81, 32, 18)])
 def test_backward_matches_float64(T1, B, A, lstm_mode):
     net, ref = _models(A, seed=1)
     ref = ref.double()
@@ -175,13 +132,15 @@ def test_backward_matches_float64(T1, B, A, lstm_mode):
     for p in ref.parameters():
         p.grad = None
     outs, _, _ = _lstm_ref(ref, x, batch["done"], state, H, whh_bf16=lstm_mode == 2)
-    core2 = _st(outs[1].reshape(n, H))
-    logits = core2 @ _st(ref.policy.weight).t() + _st(ref.policy.bias)
-    base = core2 @ _st(ref.baseline.weight).t() + _st(ref.baseline.bias)
+    st, rg = atari_ref.st_bf16, atari_ref.rg_bf16
+    core2 = st(outs[1].reshape(n, H))
+    logits = rg(core2 @ st(ref.policy.weight).t() + st(ref.policy.bias))
+    base = rg(core2 @ st(ref.baseline.weight).t() + st(ref.baseline.bias))
     torch.autograd.backward([logits, base.reshape(n)], [dl.double(), db.double()])
-    for k, p in ref.named_parameters():
-        if k.startswith("core.") or k.startswith("policy.") or k.startswith("baseline."):
-            assert rel_l2(got[k], p.grad) < 2e-2, (k, rel_l2(got[k], p.grad))
+    errs = {k: rel_l2(got[k], p.grad) for k, p in ref.named_parameters()
+            if k.startswith(("core.", "policy.", "baseline."))}
+    parity_log(f"lstm bwd T1={T1} B={B} A={A} mode={lstm_mode}", dict(grad_rel_l2=errs))
+    assert max(errs.values()) < 2e-2, errs
 
 
 def test_end_to_end_forward_and_state():
@@ -206,37 +165,6 @@ def test_autograd_backward_runs_fused_kernels():
     (out["policy_logits"].sum() + out["baseline"].pow(2).sum()).backward()
     gnorm = sum(float(p.grad.norm()) for p in net.core.parameters())
     assert gnorm > 0 and gnorm == gnorm
-
-
-@pytest.mark.parametrize("T,B,A", [(4, 5, 6), (20, 8, 18)])
-def test_learn_step_lstm_matches_upstream_restatement(T, B, A):
-    from paper_1910_03552_b200 import learner, optim
-
-    flags = dict(atari_ref.DEFAULT_FLAGS)
-    net, ref = _models(A, seed=4)
-    p0 = {k: v.detach().clone() for k, v in ref.named_parameters()}
-    ropt = torch.optim.RMSprop(ref.parameters(), lr=flags["learning_rate"], alpha=flags["alpha"],
-                               eps=flags["epsilon"])
-    opt = optim.RMSprop(net.parameters(), lr=flags["learning_rate"], alpha=flags["alpha"],
-                        eps=flags["epsilon"])
-    for step in range(2):
-        batch = _batch(T + 1, B, A, seed=20 + step)
-        state = _state(B, 513 + A, seed=30 + step)
-        total_ref, parts_ref, norm_ref = atari_ref.learn_step(ref, ropt, batch, flags, state)
-        stats = learner.learn(flags, None, net, {k: v.cuda() for k, v in batch.items()},
-                              tuple(s.cuda() for s in state), opt, None)
-        if step == 0:  # pg and baseline losses partly cancel in the total: bound by their scale
-            scale = sum(abs(float(p)) for p in parts_ref)
-            assert abs(stats["total_loss"] - total_ref) <= 1e-2 * max(1.0, scale)
-            assert abs(stats["pg_loss"] - parts_ref[0]) <= 1e-2 * abs(parts_ref[0])
-            assert abs(stats["baseline_loss"] - parts_ref[1]) <= 1e-2 * abs(parts_ref[1])
-        assert float(opt.norm) == pytest.approx(norm_ref, rel=5e-2)
-    got = net.state_dict()
-    for k, v in ref.named_parameters():
-        upd_ref = (v.detach() - p0[k]).double().reshape(1, -1)
-        upd = (got[k].detach().cpu() - p0[k]).double().reshape(1, -1)
-        cos = float(torch.nn.functional.cosine_similarity(upd, upd_ref))
-        assert cos > 0.9, (k, cos)
 
 
 def test_lstm_learn_graph_replay_is_deterministic(lstm_mode):
