@@ -273,6 +273,126 @@ def bench_lstm(dev, steps, warmup, flush, timer):
                           "mbarriers (2 layers x 81 steps forward, 2 x 81 backward)"}
 
 
+def bench_cfg4(dev, world, rank, pg, steps, barrier):
+    """configs[3]: large-batch learner step, AtariNet (no LSTM) T=80 A=18, global B=4096 sharded
+    over the ranks (B=4096/N each: strong scaling) with the NCCL SUM all-reduce.  Inputs are
+    9.4 GB of frames (> L2), so no flush is needed; graph-replayed steps, device time (CUDA
+    events on the launching stream), max over ranks."""
+    from paper_1910_03552_b200 import learner, optim
+    from paper_1910_03552_b200.atari_net import AtariNet
+
+    T, A, BG = 80, 18, 4096
+    B = BG // world
+    torch.manual_seed(99)
+    model = AtariNet(num_actions=A, device=dev)
+    opt = optim.RMSprop(model.parameters(), lr=FLAGS["learning_rate"], alpha=FLAGS["alpha"],
+                        eps=FLAGS["epsilon"])
+    batch = make_batch(T, B, A, dev, seed=300 + rank)
+    L = learner.FusedLearner(model, FLAGS, T, B, process_group=pg)
+    for _ in range(3):  # eager, capture, replay
+        L.step(batch, opt)
+    torch.cuda.synchronize()
+    barrier()
+    s = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        L.step(batch, opt)
+    e1.record(s)
+    e1.synchronize()
+    step_s = e0.elapsed_time(e1) * 1e-3 / steps
+    if world > 1:
+        t = torch.tensor([step_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_s = float(t)
+    n = (T + 1) * B
+    flops = 2 * n * (3 * sum(MACS.values()) - MACS["conv1"])  # forward + backward, per rank
+    pk = peaks()
+    tflops = flops / step_s / 1e12
+    out = {"workload": "configs[3]: AtariNet (no LSTM) learner step + RMSprop, global B=4096 "
+                       "sharded over the ranks", "T": T, "B_global": BG, "B_per_gpu": B,
+           "num_actions": A, "value": T * BG / step_s, "unit": "env-frames/s", "scaling": "strong",
+           "ms_per_step": step_s * 1e3, "steps": steps, "tflops_per_gpu": tflops,
+           "roofline": {"bound": "tensor", "achieved": tflops, "peak": pk["bf16_sustained"],
+                        "unit": "TFLOP/s", "frac": tflops / pk["bf16_sustained"],
+                        "flops_per_step_per_gpu": flops,
+                        "note": "whole step (49.5 MFLOP per frame) against the sustained bf16 peak"},
+           "l2": "inputs 9.4 GB / N > L2, no flush"}
+    del L, model, opt, batch
+    torch.cuda.empty_cache()
+    return out
+
+
+def vtrace_latency_and_cpu(timer, pk):
+    """configs[0]: vtrace.from_logits at T=20 B=32 A=6 -- latency-bound (56 KB of input), so it
+    is reported as latency: the kernel's device time per launch (steady state) and the host
+    latency of one eager `from_logits` call including the result sync.  Beside it, the CPU
+    baseline of the path: the numpy restatement of beastpipe (oracle/vtrace_np, port of
+    vtrace.py:51-128 / :224-255) on the host cores, at configs[0] and at T=80 B=4096 A=18."""
+    import numpy as np
+
+    from oracle import vtrace_np as ov
+    from paper_1910_03552_b200 import kernel_bench, vtrace
+
+    T, B, A = 20, 32, 6
+    dev_t = kernel_bench.bench_vtrace(T, B, A, timer, iters=20)
+    x = kernel_bench._vtrace_inputs(T, B, A, 0)
+    for _ in range(10):
+        vtrace.from_logits(*x)
+    torch.cuda.synchronize()
+    lat = []
+    for _ in range(200):
+        t0 = time.perf_counter()
+        r = vtrace.from_logits(*x)
+        r.vs.data_ptr()
+        torch.cuda.current_stream().synchronize()
+        lat.append(time.perf_counter() - t0)
+    lat.sort()
+
+    def cpu_time(fn, budget_s=10.0, min_reps=3):
+        ts, t_start = [], time.perf_counter()
+        while len(ts) < min_reps or time.perf_counter() - t_start < min(budget_s, 1.0):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget_s:
+                break
+        return statistics.median(ts), len(ts)
+
+    cpu = {}
+    for (t, b, a) in ((20, 32, 6), (80, 4096, 18)):
+        rng = np.random.default_rng(0)
+        beh = rng.normal(size=(t, b, a)).astype(np.float32)
+        tgt = rng.normal(size=(t, b, a)).astype(np.float32)
+        act = rng.integers(0, a, size=(t, b)).astype(np.int64)
+        disc = (np.float32(0.99) * ~(rng.random((t, b)) < 0.05)).astype(np.float32)
+        rew = rng.uniform(-1, 1, size=(t, b)).astype(np.float32)
+        val = rng.normal(size=(t, b)).astype(np.float32)
+        boot = rng.normal(size=b).astype(np.float32)
+        sec, reps = cpu_time(lambda: ov.tb_from_logits(beh, tgt, act, disc, rew, val, boot))
+        reward = rng.uniform(-1, 1, size=(t + 1, b)).astype(np.float32)
+        done = rng.random((t + 1, b)) < 0.05
+        beh_rows = rng.normal(size=(t + 1, b, a)).astype(np.float32)
+        act_rows = rng.integers(0, a, size=(t + 1, b)).astype(np.int64)
+        lbase = rng.normal(size=(t + 1, b)).astype(np.float32)
+        cfg = ov.VtraceConfig()
+        lsec, lreps = cpu_time(lambda: ov.compute_losses(reward, done, beh_rows, act_rows, tgt, lbase, cfg))
+        nbytes = kernel_bench.vtrace_bytes(t, b, a)
+        cpu[f"T{t}_B{b}_A{a}"] = {"from_logits_ms": sec * 1e3, "from_logits_gbs": nbytes / sec / 1e9,
+                                  "compute_losses_ms": lsec * 1e3, "reps": [reps, lreps]}
+    return {"from_logits_cfg0": {"T": T, "B": B, "A": A, "kernel_us": dev_t["median_s"] * 1e6,
+                                 "eager_call_us_median": lat[len(lat) // 2] * 1e6,
+                                 "eager_call_us_p10": lat[len(lat) // 10] * 1e6,
+                                 "how": "kernel: steady-state device time per launch (rotating "
+                                        "buffers, CUDA events); eager: host wall time of one "
+                                        "vtrace.from_logits call + stream sync (200 calls)"},
+            "cpu_baseline": {"kind": "port", "impl": "oracle/vtrace_np (numpy restatement of "
+                             "beastpipe action_log_rhos + vtrace_targets, compute_losses)",
+                             "cores": os.cpu_count(), "numpy_threads": os.environ.get(
+                                 "OPENBLAS_NUM_THREADS", "default"), "sizes": cpu}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -444,6 +564,11 @@ def main():
     api_s = e0.elapsed_time(e1) * 1e-3 / n_e2e
     clk.__exit__(None, None, None)
 
+    # ---- configs[3]: the large-batch learner step, strong-scaled over the ranks
+    cfg4 = None
+    if not os.environ.get("BP_BENCH_NO_CFG4"):
+        cfg4 = bench_cfg4(dev, world, rank, pg, 5, barrier)
+
     # ---- roofline of the dominant kernel group + the V-trace kernel (north-star ask)
     pk = peaks()
     br = kernel_breakdown(L, batch, opt)
@@ -490,8 +615,10 @@ def main():
                "tflops": inf_flops / ri["median_s"] / 1e12}
 
     lstm_line = None
+    vt_cfg0 = None
     if rank == 0:
         lstm_line = bench_lstm(dev, 10, 3, flush, timer)
+        vt_cfg0 = vtrace_latency_and_cpu(timer, pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -518,7 +645,7 @@ def main():
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
             "roofline": roofline, "vtrace_roofline": vt_roof,
             "learner_loss_kernel_s": ll["median_s"], "vtrace_sweep": vt_sweep,
-            "inference": inf, "lstm": lstm_line,
+            "inference": inf, "lstm": lstm_line, "cfg4": cfg4, "vtrace_cfg0": vt_cfg0,
             "cpu_baseline": cpu, "clocks": clk.summary(),
             "stats_last": {k: stats[k] for k in ("total_loss", "pg_loss", "baseline_loss",
                                                  "entropy_loss")},

@@ -206,6 +206,11 @@ typedef struct BpAtariNet {
   void* ws;     /* f32 workspace, bp_atari_workspace_bytes()  */
   size_t ws_bytes;
   int flags;    /* BP_NET_* */
+  /* nullable cudaEvent_t: the no-LSTM backward records it on the stream right after the fc
+   * weight gradient (1.6 M of the 1.69 M parameters) is final in grads, before the conv data /
+   * weight gradients -- the data-parallel learner all-reduces that bucket on a side stream
+   * while the rest of the backward runs */
+  void* fc_grad_ready;
 } BpAtariNet;
 
 /* flags: the forward does not materialise the bf16 X0 grid (conv1 reads the u8 frames on

@@ -80,7 +80,7 @@ class BpAtariNet(C.Structure):
         (name, C.c_void_p) for name in (
             "wbf", "whf", "x0", "x1", "x2", "x3", "core", "m1", "m2", "m3", "mc", "g", "d_fc",
             "d_pre3", "d_pre2", "d_pre1", "ws")
-    ] + [("ws_bytes", C.c_size_t), ("flags", C.c_int)]
+    ] + [("ws_bytes", C.c_size_t), ("flags", C.c_int), ("fc_grad_ready", C.c_void_p)]
 
 
 class BpLstmCore(C.Structure):

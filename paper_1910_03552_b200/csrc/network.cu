@@ -957,6 +957,34 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       return rc;
     }
   }
+  // fc weight gradient first (it only needs X3 and d_fc), transposed: D[k][o] = sum_n X3[n][k] d_fc[n][o] (M = 3136 features in 25
+  // m-tiles, N = 512 in 128-column tiles: one wave of 100 tiles, X3 read 4x / d_fc 25x from L2),
+  // stored transposed into grads[o][k] (per column, a warp's 32 rows are one contiguous run)
+  {
+    if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 64, 128))) return rc;
+    if ((rc = make_tmap(&tb, net->d_fc, n, 512, 64, 64, 128))) return rc;
+    GemmArgs g = base_args();
+    g.m_tiles = (3136 + 127) / 128;
+    g.n_tiles = 4;
+    g.num_kb = g.kb_per_split = (n + 63) / 64;
+    g.a_atoms_per_shift = 49;
+    g.a_nshifts = 1;
+    g.N = 512;
+    g.M = 3136;
+    g.out_f32 = 1;
+    g.out = grads + off[P_WFC];
+    g.r_img = 1;
+    g.cdiv = 1;
+    g.cq = 1;
+    g.cs1 = 3136;
+    g.col_stride = 3136;
+    if ((rc = launch_gemm<128, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    // the fc weight gradient is final: the data-parallel learner may start its all-reduce
+    if (net->fc_grad_ready && cudaEventRecord((cudaEvent_t)net->fc_grad_ready, s) != cudaSuccess) {
+      set_error("atari backward: cudaEventRecord(fc_grad_ready) failed");
+      return BP_ERR_LAUNCH;
+    }
+  }
   // conv3 dgrad: d_pre2 (conv2 10x10 grid) = sum_taps d_pre3[m - off] W3_tap^T * (X2 > 0)
   {
     const long long R = (long long)n * 81;
@@ -1116,29 +1144,6 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     }
     const int o0[1] = {0};
     if ((rc = wgrad(3, head_in, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
-  }
-  // fc weight gradient, transposed: D[k][o] = sum_n X3[n][k] d_fc[n][o] (M = 3136 features in 25
-  // m-tiles, N = 512 in 128-column tiles: one wave of 100 tiles, X3 read 4x / d_fc 25x from L2),
-  // stored transposed into grads[o][k] (per column, a warp's 32 rows are one contiguous run)
-  {
-    if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 64, 128))) return rc;
-    if ((rc = make_tmap(&tb, net->d_fc, n, 512, 64, 64, 128))) return rc;
-    GemmArgs g = base_args();
-    g.m_tiles = (3136 + 127) / 128;
-    g.n_tiles = 4;
-    g.num_kb = g.kb_per_split = (n + 63) / 64;
-    g.a_atoms_per_shift = 49;
-    g.a_nshifts = 1;
-    g.N = 512;
-    g.M = 3136;
-    g.out_f32 = 1;
-    g.out = grads + off[P_WFC];
-    g.r_img = 1;
-    g.cdiv = 1;
-    g.cq = 1;
-    g.cs1 = 3136;
-    g.col_stride = 3136;
-    if ((rc = launch_gemm<128, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
   }
   // deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
   {

@@ -104,6 +104,18 @@ class FusedLearner:
         self._seen: collections.OrderedDict = collections.OrderedDict()
         self._validated: set = set()  # graph keys whose batch schema was checked
         self._buf_gen = model.buffer_generation
+        # data parallel: the fc weight gradient (95% of the no-LSTM parameters) is all-reduced on
+        # a side stream as soon as the backward has written it (BpAtariNet.fc_grad_ready), while
+        # the conv data / weight gradients still run; the small remainder after the backward
+        self.bucketed = process_group is not None and not getattr(model, "use_lstm", False)
+        if self.bucketed:
+            names = [k for k, _ in model.named_parameters()]
+            off, cnt, _ = model._shapes[names.index("fc.weight")]
+            g = model.flat_grads
+            self._buckets = (g[off:off + cnt], g[:off], g[off + cnt:])
+            self._fc_ready = torch.cuda.Event()
+            self._fc_ready.record()  # materialise the CUDA event handle
+            self._dp_stream = torch.cuda.Stream(device=dev)
 
     def _pg_is_nccl(self) -> bool:
         """NCCL collectives can be captured in a CUDA graph; gloo ones cannot."""
@@ -251,15 +263,33 @@ class FusedLearner:
                   self.cfg, d_logits=self.d_logits[:T * B].view(T, B, A),
                   d_baseline=self.d_baseline.view(T + 1, B), losses=self.losses, status=self.status)
         # 3. backward into the flat gradient buffer
-        m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
-                            m.flat_grads, lstm=lstm)
+        if self.bucketed:
+            m._bufs.struct.fc_grad_ready = self._fc_ready.cuda_event
+        try:
+            m._backward_kernels(self.d_logits, self.d_baseline, reward.reshape(n), last_action.reshape(n),
+                                m.flat_grads, lstm=lstm)
+        finally:
+            if self.bucketed:
+                m._bufs.struct.fc_grad_ready = None
         # 4. data-parallel over B: the losses are sums over (T, B) (vtrace.py:194-196), so
-        #    the full-batch gradient is the SUM of the shard gradients (one all-reduce of the
-        #    flat f32 buffer); the loss scalars are summed too, for the stats
+        #    the full-batch gradient is the SUM of the shard gradients (all-reduce of the flat
+        #    f32 buffer); the loss scalars are summed too, for the stats and the reject check
         if self.pg is not None:
             grp = self.pg if self.pg is not True else None
-            torch.distributed.all_reduce(m.flat_grads, op=torch.distributed.ReduceOp.SUM, group=grp)
-            torch.distributed.all_reduce(self.losses, op=torch.distributed.ReduceOp.SUM, group=grp)
+            SUM = torch.distributed.ReduceOp.SUM
+            if self.bucketed:
+                fc_w, head, tail = self._buckets
+                side = self._dp_stream
+                side.wait_event(self._fc_ready)  # recorded by the backward after the fc wgrad
+                with torch.cuda.stream(side):
+                    torch.distributed.all_reduce(fc_w, op=SUM, group=grp)
+                torch.distributed.all_reduce(head, op=SUM, group=grp)
+                torch.distributed.all_reduce(tail, op=SUM, group=grp)
+                torch.distributed.all_reduce(self.losses, op=SUM, group=grp)
+                torch.cuda.current_stream().wait_stream(side)
+            else:
+                torch.distributed.all_reduce(m.flat_grads, op=SUM, group=grp)
+                torch.distributed.all_reduce(self.losses, op=SUM, group=grp)
         # 5. clip + RMSProp.  A step whose (all-reduced) total loss is non-finite -- a NaN loss,
         #    or a batch violation, which the loss kernel turns into a NaN total -- is rejected on
         #    the device (model.py:251-252: parameters untouched); stats() then raises

@@ -1,7 +1,9 @@
 """Data parallelism over B: shard gradients SUM-reduce to the full-batch gradient.
 
-CPU: the torch oracle on 2 gloo ranks.  GPU: the fused learner's all-reduce path on 2
-gloo ranks sharing one device (the NCCL path differs only in the backend name)."""
+CPU: the torch oracle on 2 gloo ranks.  GPU: the fused learner's all-reduce path on 2 ranks,
+either gloo with both ranks on cuda:0, or NCCL (graph-captured all-reduce) with one GPU per
+rank -- skipped, with the reason, when fewer than 2 GPUs are visible."""
+import functools
 import socket
 
 import pytest
@@ -18,11 +20,11 @@ def _port():
     return p
 
 
-def _run(fn, world=2):
+def _run(fn, world=2, **kw):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=fn, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=functools.partial(fn, **kw), args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     try:
@@ -59,9 +61,19 @@ def test_training_batch_shard_columns():
 
 
 @pytest.mark.gpu
-def test_fused_learner_data_parallel_matches_single_process():
-    same, cos, losses, losses1 = _run(dp_worker.fused_dp)
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_fused_learner_data_parallel_matches_single_process(backend):
+    """2 ranks x B/2 columns vs 1 process x B: the all-reduced pre-optimiser flat gradients
+    within 1e-5 relative L2 (f32 reduction order; at this size each split-K partial sums few
+    rows), identical updates on every rank, update within 1e-4 of the single-process one."""
+    import torch
+
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip(f"NCCL data parallelism needs 2 GPUs; {torch.cuda.device_count()} visible "
+                    "(gpurun leases one B200; the gloo variant covers the same learner path)")
+    same, g_rel, u_rel, losses, losses1 = _run(dp_worker.fused_dp, backend=backend)
     assert same, "every rank must apply the identical update"
-    assert cos > 0.999, cos
+    assert g_rel <= 1e-5, g_rel
+    assert u_rel <= 1e-4, u_rel
     for a, b in zip(losses, losses1):
-        assert abs(a - b) <= 1e-3 * max(1.0, abs(b))
+        assert abs(a - b) <= 1e-9 * max(1.0, abs(b))
