@@ -393,6 +393,65 @@ def vtrace_latency_and_cpu(timer, pk):
                                  "OPENBLAS_NUM_THREADS", "default"), "sizes": cpu}}
 
 
+def bench_inference(model, A, dev, timer, ks=(1, 32, 256, 1024)):
+    """configs[4]: the actor-inference loop body (pipeline.py:609-634) through the public
+    ActorInference call at dynamic batch sizes k.  Per k:
+      device_us       device time of one captured forward + fused sampling (CUDA events
+                      around graph replays, L2 flushed before each)
+      graph_call_us   host wall time of one ActorInference call on the graph path (inputs
+                      device-resident: copy into the bucket's static buffers, replay,
+                      output slices) + stream sync, median of 50
+      eager_call_us   the same on the eager path (direct kernel enqueue, any k)
+      host_roundtrip_us  pinned host observations -> H2D -> graph call -> actions D2H
+                      (what an actor-serving loop pays per batch), median of 50"""
+    from paper_1910_03552_b200.inference import ActorInference
+
+    model.eval()
+    out = {"workload": "configs[4]: AtariNet forward + fused Gumbel-max sampling (Philox), "
+                       "dynamic batch of k obs 4x84x84 u8, A=%d" % A, "per_k": {}}
+    graphs = ActorInference(model, graph_buckets=ks)
+    eager = ActorInference(model)
+    for k in ks:
+        ib = make_batch(0, k, A, dev, seed=9 + k)
+        obs = {key: ib[key] for key in ("frame", "reward", "done", "last_action")}
+        graphs(obs)
+        graph, st, _ = graphs._graphs[k]
+        rd = timer.time(graph.replay, iters=30, warmup=3, flush=True, graph=False)
+
+        def wall(fn, n=50):
+            ts = []
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            for _ in range(n):
+                t0 = time.perf_counter()
+                fn()
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t0)
+            ts.sort()
+            return ts[len(ts) // 2] * 1e6
+
+        host = {key: v.cpu().pin_memory() for key, v in obs.items()}
+        act_host = torch.empty(1, k, dtype=torch.int64).pin_memory()
+
+        def roundtrip():
+            d = {key: v.to(dev, non_blocking=True) for key, v in host.items()}
+            o, _ = graphs(d)
+            act_host.copy_(o["action"], non_blocking=True)
+
+        flops = 2 * k * sum(MACS.values())
+        out["per_k"][str(k)] = {
+            "device_us": rd["median_s"] * 1e6, "obs_per_s": k / rd["median_s"],
+            "tflops": flops / rd["median_s"] / 1e12,
+            "graph_call_us": wall(lambda: graphs(obs)), "eager_call_us": wall(lambda: eager(obs)),
+            "host_roundtrip_us": wall(roundtrip),
+            "h2d_bytes": sum(v.numel() * v.element_size() for v in host.values()), "d2h_bytes": 8 * k}
+    model.train()
+    big = out["per_k"][str(ks[-1])]
+    out.update(ms=big["device_us"] * 1e-3, obs_per_s=big["obs_per_s"], tflops=big["tflops"])
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -598,21 +657,11 @@ def main():
         rl = kernel_bench.bench_loss(80, bb, 18, timer, iters=10)
         vt_sweep[str(bb)] = {"vtrace_gbs": r["gbs"], "vtrace_frac": r["gbs"] / pk["hbm"],
                              "loss_gbs": rl["gbs"], "loss_frac": rl["gbs"] / pk["hbm"]}
-    # configs[4]: actor-inference forward (PolyBeast dynamic batching) on 1024 observations,
-    # forward + Gumbel-max action sampling, CUDA-graphed
+    # configs[4]: actor-inference forward (PolyBeast dynamic batching): forward + fused
+    # Gumbel-max sampling per dynamic batch of k observations
     inf = None
     if rank == 0:
-        ib = make_batch(0, 1024, A, dev, seed=9)
-        inputs = {k: ib[k] for k in ("frame", "reward", "done", "last_action")}
-        model.eval()
-        with torch.no_grad():
-            fwd = lambda: model(inputs)  # noqa: E731
-            ri = timer.time(fwd, iters=20, warmup=3, flush=True, graph=True)
-        model.train()
-        inf_flops = 2 * 1024 * sum(MACS.values())
-        inf = {"workload": "configs[4]: AtariNet forward + sampling, 1024 obs 4x84x84",
-               "ms": ri["median_s"] * 1e3, "obs_per_s": 1024 / ri["median_s"],
-               "tflops": inf_flops / ri["median_s"] / 1e12}
+        inf = bench_inference(model, A, dev, timer)
 
     lstm_line = None
     vt_cfg0 = None

@@ -265,6 +265,17 @@ int bp_atari_set_wgrad_window(int on);
 int bp_atari_forward_planes(const BpAtariNet* net, int n, const uint8_t* planes, const int32_t* plane_index,
                             int num_planes, const float* reward, const int64_t* last_action,
                             const float* params, float* logits, float* baseline, void* stream);
+/* Actor inference (the PolyBeast / beastpipe inference loop body, pipeline.py:609-634:
+ * mlp_forward + sample_actions): bp_atari_forward / bp_atari_forward_planes (plane_index
+ * nullable) whose heads-GEMM epilogue also draws actions [n] int64 (Gumbel-max over the
+ * row's logits in registers, same RNG and draws as bp_sample_actions_f32; greedy != 0 ->
+ * argmax).  n is any batch size (the dynamic batch k).  seed_state (nullable) makes the
+ * key device-resident for CUDA-graph replays: the call first advances *seed_state by one
+ * splitmix64 step, then draws with the advanced value (seed is ignored). */
+int bp_atari_forward_sample(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
+                            int num_planes, const float* reward, const int64_t* last_action,
+                            const float* params, uint64_t seed, uint64_t* seed_state, int greedy, float* logits, float* baseline,
+                            int64_t* actions, void* stream);
 /* Backward of the last forward: d_logits [n][A], d_baseline [n] -> grads (flat f32,
  * same layout as params; every entry is overwritten). */
 int bp_atari_backward(const BpAtariNet* net, int n, const float* d_logits, const float* d_baseline,
@@ -332,6 +343,14 @@ int bp_atari_lstm_forward_planes(const BpAtariNet* net, const BpLstmCore* core, 
                                  const float* reward, const int64_t* last_action, const uint8_t* done,
                                  const float* params, const float* h0, const float* c0, float* logits,
                                  float* baseline, float* hN, float* cN, void* stream);
+/* bp_atari_lstm_forward (plane_index nullable) with the fused action sampling of
+ * bp_atari_forward_sample; T1 = 1 is the actor's per-step core_state update. */
+int bp_atari_lstm_forward_sample(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                 const uint8_t* frames, const int32_t* plane_index, int num_planes,
+                                 const float* reward, const int64_t* last_action, const uint8_t* done,
+                                 const float* params, const float* h0, const float* c0, uint64_t seed,
+                                 uint64_t* seed_state, int greedy, float* logits, float* baseline, float* hN, float* cN,
+                                 int64_t* actions, void* stream);
 /* Backward of the last bp_atari_lstm_forward (same T1, B, done, c0): d_logits [N][A],
  * d_baseline [N] -> grads (flat, every entry overwritten).  The initial state gets no
  * gradient (upstream learn() feeds the actors' state as a constant). */
@@ -339,10 +358,11 @@ int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1
                            const float* d_logits, const float* d_baseline, const uint8_t* done,
                            const float* params, const float* c0, float* grads, void* stream);
 
-/* Categorical sampling per row (Gumbel-max, counter-based hash RNG keyed by
- * (seed, row, column)); greedy != 0 -> argmax.  Replaces sample_actions
- * (model.py:218-221) / upstream torch.multinomial(softmax(logits)).
- * logits [n][A] f32 -> actions [n] int64. */
+/* Categorical sampling per row (Gumbel-max; Philox4x32-10 keyed by the 64-bit seed,
+ * counter (row, column / 4) -> word column % 4, u = ((w >> 8) + 1/2) 2^-24, noise
+ * -log(-log u)); greedy != 0 -> argmax.  Replaces sample_actions (model.py:218-221) /
+ * upstream torch.multinomial(softmax(logits)).  logits [n][A] f32 -> actions [n] int64.
+ * Draws are identical to the fused sampler of bp_atari_forward_sample for the same seed. */
 int bp_sample_actions_f32(const float* logits, int n, int A, uint64_t seed, int greedy,
                           int64_t* actions, void* stream);
 /* Infeed slot refill (DeviceInfeed.put; the reference stacks rollouts on the host,

@@ -62,6 +62,9 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_lstm_forward_planes": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),
     "bp_sample_actions_f32": (I, [P, I, I, C.c_uint64, I, P, P]),
+    "bp_atari_forward_sample": (I, [P, I, P, P, I, P, P, P, C.c_uint64, P, I, P, P, P, P]),
+    "bp_atari_lstm_forward_sample": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, C.c_uint64, P, I,
+                                         P, P, P, P, P, P]),
     "bp_pack_stats": (I, [P, P, P, I, P, P, P]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),
     "bp_infeed_get": (I, [P, P, P]),

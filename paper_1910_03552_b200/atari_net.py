@@ -294,17 +294,19 @@ class AtariNet(nn.Module):
 
     def _forward_kernels(self, frames, reward, last_action, logits=None, baseline=None,
                          repack: bool | None = None, lstm: dict | None = None, plane_index=None,
-                         keep_x0: bool = True):
+                         keep_x0: bool = True, actions=None, seed: int = 0, greedy: bool = False,
+                         seed_state=None):
         """frames u8 (n,4,84,84), reward f32 (n,), last_action i64 (n,) -> logits, baseline.
 
         Frame-stack dedup: with plane_index (n,4) int32, `frames` is a plane store
         (P,84,84) u8 and channel c of frame i is frames[plane_index[i, c]]
         (rollout.frame_stack_index builds the upstream FrameStack indexing).
-        repack=None packs the bf16 mirror only when stale; False trusts it (the fused
-        optimiser step keeps it fresh); True always packs.  LSTM nets take
+        repack=None packs the bf16 mirror only when stale; False trusts its version (the fused
+        optimiser step keeps it fresh) but still packs a never-packed buffer set; True always packs.  LSTM nets take
         lstm=dict(T1, B, done u8 (n,), h0, c0 (2,B,H) f32[, hN, cN]); the final state
         is returned in lstm["hN"], lstm["cN"].  keep_x0=False (inference without a backward)
-        skips conv1's X0 side output."""
+        skips conv1's X0 side output.  actions (n,) int64: the heads epilogue also draws the
+        actions (Gumbel-max with `seed`, or argmax when greedy; same draws as sample())."""
         if plane_index is not None:
             if plane_index.dtype != torch.int32 or plane_index.shape[-1] != 4:
                 raise DimensionError("plane_index must be int32 (n, 4)")
@@ -316,7 +318,8 @@ class AtariNet(nn.Module):
         else:
             n = frames.shape[0]
         b = self.buffers_for(n)
-        if repack or (repack is None and self.mirror_stale()):
+        # (a freshly (re)allocated buffer set has no mirror yet: packed even with repack=False)
+        if repack or not self.mirror_fresh or (repack is None and self.mirror_stale()):
             self.pack_weights()
         if logits is None:
             logits = torch.empty(n, self.num_actions, device=frames.device)
@@ -337,7 +340,16 @@ class AtariNet(nn.Module):
             tail = (N.ptr(reward), N.ptr(last_action), N.ptr(lstm["done"]), N.ptr(self.flat_params),
                     N.ptr(lstm["h0"]), N.ptr(lstm["c0"]), N.ptr(logits), N.ptr(baseline),
                     N.ptr(lstm["hN"]), N.ptr(lstm["cN"]), stream)
-            if plane_index is not None:
+            if actions is not None:
+                idx = N.ptr(plane_index) if plane_index is not None else None
+                np_ = num_planes if plane_index is not None else 0
+                N.check(N.lib().bp_atari_lstm_forward_sample(
+                    b.ref, b.lstm.ref, T1, B, N.ptr(frames), idx, np_, N.ptr(reward), N.ptr(last_action),
+                    N.ptr(lstm["done"]), N.ptr(self.flat_params), N.ptr(lstm["h0"]), N.ptr(lstm["c0"]),
+                    seed, N.ptr(seed_state) if seed_state is not None else None, int(greedy), N.ptr(logits),
+                    N.ptr(baseline), N.ptr(lstm["hN"]), N.ptr(lstm["cN"]),
+                    N.ptr(actions), stream), "bp_atari_lstm_forward_sample")
+            elif plane_index is not None:
                 N.check(N.lib().bp_atari_lstm_forward_planes(
                     b.ref, b.lstm.ref, T1, B, N.ptr(frames), N.ptr(plane_index), num_planes, *tail),
                     "bp_atari_lstm_forward_planes")
@@ -347,7 +359,15 @@ class AtariNet(nn.Module):
         else:
             tail = (N.ptr(reward), N.ptr(last_action), N.ptr(self.flat_params), N.ptr(logits),
                     N.ptr(baseline), stream)
-            if plane_index is not None:
+            if actions is not None:
+                idx = N.ptr(plane_index) if plane_index is not None else None
+                np_ = num_planes if plane_index is not None else 0
+                N.check(N.lib().bp_atari_forward_sample(
+                    b.ref, n, N.ptr(frames), idx, np_, N.ptr(reward), N.ptr(last_action),
+                    N.ptr(self.flat_params), seed, N.ptr(seed_state) if seed_state is not None else None,
+                    int(greedy), N.ptr(logits), N.ptr(baseline),
+                    N.ptr(actions), stream), "bp_atari_forward_sample")
+            elif plane_index is not None:
                 N.check(N.lib().bp_atari_forward_planes(b.ref, n, N.ptr(frames), N.ptr(plane_index),
                                                         num_planes, *tail), "bp_atari_forward_planes")
             else:
@@ -378,12 +398,17 @@ class AtariNet(nn.Module):
                                                  N.ptr(d_logits), N.ptr(d_baseline), N.ptr(grads), stream),
                 "bp_atari_backward_frames")
 
-    def sample(self, logits: torch.Tensor, greedy: bool) -> torch.Tensor:
+    def next_sample_seed(self) -> int:
+        """Per-call 64-bit Philox key of the action sampler (sample_seed, call counter)."""
+        self._calls += 1
+        return (self.sample_seed * 0x9E3779B97F4A7C15 + self._calls) & 0xFFFFFFFFFFFFFFFF
+
+    def sample(self, logits: torch.Tensor, greedy: bool, seed: int | None = None) -> torch.Tensor:
         """Gumbel-max categorical sample (training) or argmax (eval), one kernel."""
         n = logits.shape[0]
         out = torch.empty(n, dtype=torch.int64, device=logits.device)
-        self._calls += 1
-        seed = (self.sample_seed * 0x9E3779B97F4A7C15 + self._calls) & 0xFFFFFFFFFFFFFFFF
+        if seed is None:
+            seed = self.next_sample_seed()
         N.check(N.lib().bp_sample_actions_f32(N.ptr(logits), n, self.num_actions, seed, int(greedy),
                                               N.ptr(out), N.stream_handle(logits.device)),
                 "bp_sample_actions_f32")
@@ -423,16 +448,21 @@ class AtariNet(nn.Module):
             if torch.is_grad_enabled():
                 logits, baseline, hN, cN = _AtariLstmFunction.apply(
                     self, frames, reward, last_action, done, h0, c0, T, B, *self.parameters())
-            else:
+            else:  # inference: the heads epilogue samples the actions
                 lstm = dict(T1=T, B=B, done=done, h0=h0, c0=c0)
-                logits, baseline = self._forward_kernels(frames, reward, last_action, lstm=lstm)
+                action = torch.empty(T * B, dtype=torch.int64, device=frames.device)
+                logits, baseline = self._forward_kernels(frames, reward, last_action, lstm=lstm, actions=action,
+                                                         seed=self.next_sample_seed(), greedy=not self.training)
                 hN, cN = lstm["hN"], lstm["cN"]
             state = (hN, cN)
         elif torch.is_grad_enabled():
             logits, baseline = _AtariFunction.apply(self, frames, reward, last_action,
                                                     *self.parameters())
-        else:  # inference: no backward follows, conv1 skips the X0 side output
-            logits, baseline = self._forward_kernels(frames, reward, last_action, keep_x0=False)
-        action = self.sample(logits.detach(), greedy=not self.training)
+        else:  # inference: no backward follows (conv1 skips the X0 side output), fused sampling
+            action = torch.empty(T * B, dtype=torch.int64, device=frames.device)
+            logits, baseline = self._forward_kernels(frames, reward, last_action, keep_x0=False, actions=action,
+                                                     seed=self.next_sample_seed(), greedy=not self.training)
+        if torch.is_grad_enabled():
+            action = self.sample(logits.detach(), greedy=not self.training)
         return (dict(policy_logits=logits.view(T, B, self.num_actions), baseline=baseline.view(T, B),
                      action=action.view(T, B)), state)

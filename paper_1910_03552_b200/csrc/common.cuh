@@ -144,4 +144,56 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// ---------------------------------------------------------------------------
+// Action sampling: Gumbel-max with Philox4x32-10 (Salmon et al., SC'11) keyed by the
+// 64-bit seed, counter (row lo, row hi, column / 4, 0) -> word column % 4.  The standalone
+// sampler (bp_sample_actions_f32) and the heads-GEMM epilogue share these functions, so
+// both draw the same action for the same (seed, row) (sample_actions model.py:218-221).
+// ---------------------------------------------------------------------------
+BP_DEVICE uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Gumbel(0, 1) noise of uniform word w: u = (w >> 8 + 1/2) 2^-24 in (0, 1), -log(-log u)
+BP_DEVICE float gumbel_of(uint32_t w) {
+  const float u = ((float)(w >> 8) + 0.5f) * (1.0f / 16777216.0f);
+  return -logf(-logf(u));
+}
+
+// argmax_j (logit_j + Gumbel_j) over the first A values of a row (greedy: argmax logit_j);
+// ties and NaNs resolve to the lowest index, as np.argmax on finite inputs
+template <int MAXA>
+BP_DEVICE int gumbel_argmax(const float* v, int A, unsigned long long seed, unsigned long long row, bool greedy) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  float best = -INFINITY;
+  int arg = 0;
+#pragma unroll
+  for (int j0 = 0; j0 < MAXA; j0 += 4) {
+    if (j0 >= A) break;
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (!greedy) w = philox4x32_10(make_uint4((uint32_t)row, (uint32_t)(row >> 32), (uint32_t)(j0 >> 2), 0u), key);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      if (j < A) {
+        const float x = greedy ? v[j] : v[j] + gumbel_of(ws[q]);
+        if (x > best) {
+          best = x;
+          arg = j;
+        }
+      }
+    }
+  }
+  return arg;
+}
+
 }  // namespace bp

@@ -819,8 +819,30 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
 }
 
 // heads: head_in [n, 576] ([core | 1 | 0]) x Whf [32, 576] -> logits [n, A], baseline [n]
+// fused action sampling of the heads epilogue (inference: bp_atari_forward_sample)
+struct SampleSpec {
+  int64_t* actions;
+  unsigned long long seed;
+  unsigned long long* seed_state;  // device-resident seed (graph replays): advanced per call
+  int greedy;
+};
+
+// graph-replayable sampling: every call advances the device-resident seed (splitmix64 step)
+__global__ void advance_seed_kernel(unsigned long long* seed_state) {
+  unsigned long long x = *seed_state + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  *seed_state = x ^ (x >> 31);
+}
+
+static int advance_seed(const SampleSpec* smp, cudaStream_t s) {
+  if (!smp || !smp->seed_state) return BP_OK;
+  advance_seed_kernel<<<1, 1, 0, s>>>(smp->seed_state);
+  return check_launch("advance_seed_kernel");
+}
+
 static int heads_forward(const BpAtariNet* net, int n, const void* head_in, float* logits, float* baseline,
-                         cudaStream_t s) {
+                         cudaStream_t s, const SampleSpec* smp = nullptr) {
   CUtensorMap ta, tb;
   int rc;
   if ((rc = make_tmap(&ta, head_in, n, kCoreW, 64, 128, 128))) return rc;
@@ -836,6 +858,12 @@ static int heads_forward(const BpAtariNet* net, int n, const void* head_in, floa
   g.A = net->num_actions;
   g.logits = logits;
   g.baseline = baseline;
+  if (smp) {
+    g.actions = smp->actions;
+    g.sample_seed = smp->seed;
+    g.seed_state = smp->seed_state;
+    g.greedy = smp->greedy;
+  }
   return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s);
 }
 
@@ -849,7 +877,7 @@ static int check_planes(const uint8_t* planes, const int32_t* plane_index, int n
 
 static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
                          int num_planes, const float* reward, const int64_t* last_action, const float* params,
-                         float* logits, float* baseline, void* stream) {
+                         float* logits, float* baseline, void* stream, const SampleSpec* smp = nullptr) {
   if (int e = check_net(net, n)) return e;
   if (int e = check_planes(frames, plane_index, num_planes)) return e;
   if (net->use_lstm) {
@@ -860,9 +888,10 @@ static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 0, off);
   int rc;
+  if ((rc = advance_seed(smp, s))) return rc;
   if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
     return rc;
-  return heads_forward(net, n, net->core, logits, baseline, s);
+  return heads_forward(net, n, net->core, logits, baseline, s, smp);
 }
 
 extern "C" int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames,
@@ -881,6 +910,21 @@ extern "C" int bp_atari_forward_planes(const BpAtariNet* net, int n, const uint8
   }
   return atari_forward(net, n, planes, plane_index, num_planes, reward, last_action, params, logits, baseline,
                        stream);
+}
+
+extern "C" int bp_atari_forward_sample(const BpAtariNet* net, int n, const uint8_t* frames,
+                                       const int32_t* plane_index, int num_planes, const float* reward,
+                                       const int64_t* last_action, const float* params, uint64_t seed,
+                                       uint64_t* seed_state, int greedy, float* logits, float* baseline, int64_t* actions,
+                                       void* stream) {
+  if (!actions) {
+    set_error("atari: bp_atari_forward_sample needs an actions buffer");
+    return BP_ERR_ARG;
+  }
+  const SampleSpec smp{actions, (unsigned long long)seed, reinterpret_cast<unsigned long long*>(seed_state),
+                       greedy};
+  return atari_forward(net, n, frames, plane_index, plane_index ? num_planes : 0, reward, last_action, params,
+                       logits, baseline, stream, &smp);
 }
 
 // G = [d_logits | d_baseline | 0] bf16, then the heads data-gradient:
@@ -1327,7 +1371,8 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
                               const uint8_t* frames, const int32_t* plane_index, int num_planes,
                               const float* reward, const int64_t* last_action, const uint8_t* done,
                               const float* params, const float* h0, const float* c0, float* logits,
-                              float* baseline, float* hN, float* cN, void* stream) {
+                              float* baseline, float* hN, float* cN, void* stream,
+                              const SampleSpec* smp = nullptr) {
   if (int e = check_lstm(net, core, T1, B)) return e;
   if (int e = check_planes(frames, plane_index, num_planes)) return e;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1335,6 +1380,7 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 1, off);
   int rc;
+  if ((rc = advance_seed(smp, s))) return rc;
   if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
     return rc;
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(core->wih);
@@ -1396,7 +1442,7 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
       if ((rc = cl ? lstm_cl_launch_fwd(a, s) : lstm_launch_fwd(a, s))) return rc;
     }
   }
-  return heads_forward(net, n, bfp(core->out, 1), logits, baseline, s);
+  return heads_forward(net, n, bfp(core->out, 1), logits, baseline, s, smp);
 }
 
 extern "C" int bp_atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
@@ -1420,6 +1466,24 @@ extern "C" int bp_atari_lstm_forward_planes(const BpAtariNet* net, const BpLstmC
   }
   return atari_lstm_forward(net, core, T1, B, planes, plane_index, num_planes, reward, last_action, done, params,
                             h0, c0, logits, baseline, hN, cN, stream);
+}
+
+extern "C" int bp_atari_lstm_forward_sample(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
+                                            const uint8_t* frames, const int32_t* plane_index, int num_planes,
+                                            const float* reward, const int64_t* last_action,
+                                            const uint8_t* done, const float* params, const float* h0,
+                                            const float* c0, uint64_t seed, uint64_t* seed_state,
+                                            int greedy, float* logits,
+                                            float* baseline, float* hN, float* cN, int64_t* actions,
+                                            void* stream) {
+  if (!actions) {
+    set_error("atari: bp_atari_lstm_forward_sample needs an actions buffer");
+    return BP_ERR_ARG;
+  }
+  const SampleSpec smp{actions, (unsigned long long)seed, reinterpret_cast<unsigned long long*>(seed_state),
+                       greedy};
+  return atari_lstm_forward(net, core, T1, B, frames, plane_index, plane_index ? num_planes : 0, reward,
+                            last_action, done, params, h0, c0, logits, baseline, hN, cN, stream, &smp);
 }
 
 extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* core, int T1, int B,
@@ -1516,28 +1580,30 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
 
 // ============================================================ action sampling
 namespace bp {
-BP_DEVICE uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
+// same draw as the fused heads epilogue (gumbel_argmax, common.cuh) for any A
 __global__ void sample_actions_kernel(const float* __restrict__ logits, int n, int A, uint64_t seed,
                                       int greedy, int64_t* __restrict__ actions) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
+  const float* row = logits + (size_t)r * A;
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   float best = -INFINITY;
   int arg = 0;
-  for (int j = 0; j < A; ++j) {
-    float v = logits[(size_t)r * A + j];
-    if (!greedy) {
-      const uint64_t h = mix64(seed ^ mix64(((uint64_t)r << 8) | (uint64_t)j));
-      const float u = ((float)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
-      v += -logf(-logf(u));  // Gumbel(0, 1)
-    }
-    if (v > best) {
-      best = v;
-      arg = j;
+  for (int j0 = 0; j0 < A; j0 += 4) {
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (!greedy) w = philox4x32_10(make_uint4((uint32_t)r, 0u, (uint32_t)(j0 >> 2), 0u), key);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      if (j < A) {
+        const float v = row[j];
+        const float x = greedy ? v : v + gumbel_of(ws[q]);
+        if (x > best) {
+          best = x;
+          arg = j;
+        }
+      }
     }
   }
   actions[r] = arg;

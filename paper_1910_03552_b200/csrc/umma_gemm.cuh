@@ -85,6 +85,10 @@ struct GemmArgs {
   int heads, A;
   float* logits;   // [M][A] f32
   float* baseline; // [M] f32
+  int64_t* actions;          // heads: optional fused Gumbel-max action per row (null = none)
+  unsigned long long sample_seed;
+  const unsigned long long* seed_state;  // non-null: the seed is read from device memory
+  int greedy;                // heads sampling: argmax instead of Gumbel-max
   // AU8 (conv1): the A operand is built on chip from u8 frames instead of a bf16 grid.
   // Grid row r = img*441 + gy*21 + gx, channel ci*16 + ry*4 + rx of row r is
   // frame(img, ci)[4gy + ry][4gx + rx]; frame(img, ci) = u8 + plane * 7056 with
@@ -280,6 +284,8 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
         if (n0 + j < g.A) g.logits[(size_t)m * g.A + n0 + j] = v[j];
         else if (n0 + j == g.A) g.baseline[m] = v[j];
       }
+      // fused sampling: the whole row (A + 1 <= 32 columns) is in this thread's registers
+      if (g.actions && n0 == 0) g.actions[m] = gumbel_argmax<32>(v, g.A, g.seed_state ? *g.seed_state : g.sample_seed, (unsigned long long)m, g.greedy != 0);
     }
     return;
   }
