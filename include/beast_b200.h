@@ -305,7 +305,8 @@ typedef struct BpLstmCore {
   int max_rows;   /* capacity N = T1 * B */
   void* wih;      /* [2][G4][576] bf16 [W_ih | b_ih + b_hh | 0], rows >= 4H zero   */
   float* gx;      /* [N][G4] input projection of the current layer            */
-  float* gates;   /* [2][N][4H] activated gates i, f, g, o                   */
+  float* gates;   /* [2][N][8H] per-step gate records (cluster path: [N][H][8]
+                     {i, f, g, o, c, pad} f32; cooperative path: [N][4H] i,f,g,o) */
   float* cseq;    /* [2][N][H] cell states                                   */
   void* hprev;    /* [2][N][576] bf16 [notdone_t h_{t-1} | 1 | 0], zeroed once */
   void* out;      /* [2][N][576] bf16 [h_t | 1 | 0], zeroed once; out[1] feeds the heads */

@@ -72,7 +72,7 @@ class _LstmBuffers:
         self.t = dict(
             wih=torch.empty(2, G4, 576, dtype=bf, device=d),
             gx=torch.empty(n, G4, dtype=f32, device=d),
-            gates=torch.empty(2, n, 4 * H, dtype=f32, device=d),
+            gates=torch.empty(2, n, 8 * H, dtype=f32, device=d),
             cseq=torch.empty(2, n, H, dtype=f32, device=d),
             # padding columns of these are never written: zero once
             hprev=torch.zeros(2, n, 576, dtype=bf, device=d),

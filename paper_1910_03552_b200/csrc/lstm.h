@@ -20,22 +20,24 @@ struct LstmFwdArgs {
   const float* h0;            // [ldb][H]
   const float* c0;            // [ldb][H]
   float* hx;                  // [2][H][kLstmB] exchange (per chunk)
-  float* gates;               // [rows][4H] activated i, f, g, o
-  float* cseq;                // [rows][H]
+  float* gates;               // cooperative path: [rows][4H] activated i, f, g, o
+  float* cseq;                // cooperative path: [rows][H]
+  float* act8;                // cluster path: [rows][H][8] f32 {i, f, g, o, c, -, -, -}
   __nv_bfloat16* out_aug;     // [rows][aug_ld]: [h_t | 1 | 0]
   __nv_bfloat16* hprev_aug;   // [rows][aug_ld]: [notdone_t * h_{t-1} | 1 | 0]
   int aug_ld;
   float* hN;                  // [ldb][H]
   float* cN;                  // [ldb][H]
-  int dbg;                    // diagnostics: bit 0 skip owner global stores, bit 1 skip MMAs
+  int dbg;                    // diagnostics: bit 0 skip the step-output stores, bit 1 skip MMAs
   const uint32_t* wfrag;      // cluster path: packed forward A-fragments (lstm_cl_pack)
 };
 
 struct LstmBwdArgs {
   int H, B, ldb, b0, T1;
   const float* whh;
-  const float* gates;
+  const float* gates;         // cooperative path (as LstmFwdArgs)
   const float* cseq;
+  const float* act8;          // cluster path (as LstmFwdArgs)
   const float* c0;
   const uint8_t* done;
   const float* dh_out;        // [rows][dh_ld] gradient w.r.t. the layer output h_t

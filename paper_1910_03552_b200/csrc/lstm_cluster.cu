@@ -22,6 +22,7 @@
 // the recurrent critical path.
 #include "common.cuh"
 #include "lstm.h"
+#include "tma_host.h"
 
 namespace bp {
 
@@ -103,12 +104,12 @@ constexpr uint32_t BWD_SLICE = UC * NB * 4;           // bytes of one CTA's part
 constexpr int OWNERS = UC * NB;                       // 272 owner threads (warps 0..8)
 
 struct FwdSmem {
+  float rec[2][NB][UC][8];               // step records {i, f, g, o, c, -} by step parity: the
+                                         // box of one 4D TMA store (act8, [rows][H][8])
   __nv_bfloat16 h[NB][KPS];              // MMA operand h_{t-1}: [batch][unit]
   __nv_bfloat16 in[2][CS][NB][SL];       // incoming slices: [parity][source CTA][batch][unit]
   __nv_bfloat16 out[NB][SL];             // this CTA's new h slice
   float red[4][MT * 16][NB];             // per K-quarter partial pre-gates
-  float act[2][NB][5][UC];               // step outputs by step parity: i f g o c
-  __nv_bfloat16 hb[2][2][NB][UC];        // h_t, notdone_t * h_{t-1} (bf16 sequences), by parity
   uint64_t bar[2];                       // incoming-slice barriers, by step parity
 };
 
@@ -120,6 +121,14 @@ struct BwdSmem {
 };
 
 // shared::cta -> shared::cluster bulk copy completing on the destination CTA's mbarrier
+// 4D tensor store of a step-record box (smem -> global, bulk async-group of the issuing thread)
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src, int x, int y, int z, int w) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
@@ -142,14 +151,14 @@ int lstm_cl_set_trace(void* buf) {
 // dataflow orders buffer reuse (a CTA cannot send step t+2 before it has received every
 // CTA's step t+1, which each CTA sends only after it consumed step t), so there is no
 // cluster-wide barrier inside the loop.
-__global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_constant__ LstmFwdArgs a,
+                                                                  const __grid_constant__ CUtensorMap tm_rec) {
   extern __shared__ __align__(128) unsigned char smraw[];
   FwdSmem& S = *reinterpret_cast<FwdSmem*>(smraw);
-  const int H = a.H, H4 = 4 * H;
+  const int H = a.H;
   const int rank = (int)cluster_rank();
   const int cb = (blockIdx.x / CS) * NB;  // first batch column of this cluster (within the pass)
   const int u0 = rank * UC;
-  const int nu = H - u0 < UC ? H - u0 : UC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tig = lane & 3;
   unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_cl_trace : nullptr;
   if (trace) trace[4 * a.T1 * 2] = gtimer();
@@ -186,6 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
   const int col = cb + ob;
   const bool owner = tid < OWNERS && j < H && col < a.B;
   float c = 0.f, hown = 0.f, gxn[4] = {0.f, 0.f, 0.f, 0.f};
+  __nv_bfloat16 hb_out = __float2bfloat16_rn(0.f), hb_prev = hb_out;  // this step's bf16 sequence values
   bool donen = false;
   if (owner) {
     const size_t row = (size_t)a.b0 + col;
@@ -203,35 +213,14 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
   const int ncols = a.B - cb < NB ? a.B - cb : NB;
   cluster_sync_all();  // every CTA running, barriers initialised, before any DSMEM traffic
   if (trace) trace[4 * a.T1 * 2 + 1] = gtimer();
-  // the outputs of step tt (staged in smem by parity), coalesced along the CTA's 34 units and
-  // written by every thread: issued at the top of step tt + 1, where the stores overlap the
-  // latency-bound recurrent MMAs instead of sitting before the exchange wait
-  auto store_step = [&](int tt) {
-    if (a.dbg & 1) return;
-    const int pp = tt & 1;
-    const size_t trow = (size_t)tt * a.ldb + a.b0 + cb;
-    // one (batch, quantity) segment of the CTA's units per warp: warp-uniform branches
-    for (int sg = warp; sg < ncols * 7; sg += WARPS) {
-      const int b = sg / 7, k = sg - b * 7;
-      const size_t row = trow + b;
-      for (int u = lane; u < nu; u += 32) {
-        if (k < 4) a.gates[row * H4 + (size_t)k * H + u0 + u] = S.act[pp][b][k][u];
-        else if (k == 4) a.cseq[row * H + u0 + u] = S.act[pp][b][4][u];
-        else if (k == 5) a.out_aug[row * a.aug_ld + u0 + u] = S.hb[pp][0][b][u];
-        else a.hprev_aug[row * a.aug_ld + u0 + u] = S.hb[pp][1][b][u];
-      }
-    }
-    if (rank == 0 && tid < ncols) {  // bias (ones) column of both augmented rows
-      const size_t row = trow + tid;
-      a.out_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
-      a.hprev_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
-    }
-  };
-
+  // the step records {i, f, g, o, c} leave through one 4D TMA store per step (issued by thread
+  // STORE_TID, asynchronous: no global-store instructions on the recurrent critical path); the
+  // bf16 sequences (h_t, notdone_t h_{t-1}) are stored by the owners directly
+  constexpr int STORE_TID = 32;
+  if (tid == STORE_TID) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rec)) : "memory");
   for (int t = 0; t < a.T1; ++t) {
     const int p = t & 1;
     if (trace) trace[t * 4 + 0] = gtimer();
-    if (t > 0) store_step(t - 1);
     // ---- recurrent pre-gates W_hh h_{t-1}: 3 independent accumulator chains per warp
     {
       float acc[ITEMS][4];
@@ -261,6 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
       }
     }
     if (tid < CS) bulk_wait_read_all();  // the previous step's slice copies have read S.out
+    if (tid == STORE_TID) bulk_wait_read_1();  // step t-2's record store has read S.rec[p]
     __syncthreads();
     if (trace) trace[t * 4 + 1] = gtimer();
     if (owner) {
@@ -283,20 +273,29 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
       const float h = og * tanh_fast(c);
       const __nv_bfloat16 hb = __float2bfloat16_rn(h);
       S.out[ob][ou] = hb;
-      S.act[p][ob][0][ou] = ig;
-      S.act[p][ob][1][ou] = fg;
-      S.act[p][ob][2][ou] = gg;
-      S.act[p][ob][3][ou] = og;
-      S.act[p][ob][4][ou] = c;
-      S.hb[p][0][ob][ou] = hb;
-      S.hb[p][1][ob][ou] = __float2bfloat16_rn(nd * hown);
+      if (!(a.dbg & 1)) {
+        *reinterpret_cast<float4*>(&S.rec[p][ob][ou][0]) = make_float4(ig, fg, gg, og);
+        S.rec[p][ob][ou][4] = c;
+        fence_proxy_async_smem();  // generic writes -> the TMA store (async proxy)
+      }
+      hb_out = hb;
+      hb_prev = __float2bfloat16_rn(nd * hown);
       hown = h;
       if (t == a.T1 - 1) {
         a.hN[(size_t)(a.b0 + col) * H + j] = h;
         a.cN[(size_t)(a.b0 + col) * H + j] = c;
       }
     }
+    if (rank == 0 && tid < ncols && !(a.dbg & 1)) {  // bias (ones) column of both augmented rows
+      const size_t row = (size_t)t * a.ldb + a.b0 + cb + tid;
+      a.out_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
+      a.hprev_aug[row * a.aug_ld + H] = __float2bfloat16_rn(1.f);
+    }
     __syncthreads();
+    if (tid == STORE_TID && !(a.dbg & 1)) {
+      tma_store_4d(&tm_rec, smem_u32(&S.rec[p][0][0][0]), 0, u0, a.b0 + cb, t);
+      bulk_commit();
+    }
     if (trace) trace[t * 4 + 2] = gtimer();
     const bool exch = t + 1 < a.T1;
     // ---- exchange: own slice -> every CTA's in[p][rank] (bulk DSMEM copies, one per lane)
@@ -308,6 +307,12 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
                        FWD_SLICE, mapa(smem_u32(&S.bar[p]), (uint32_t)lane));
         bulk_commit();
       }
+    }
+    // the bf16 sequences: stored while the slices travel (off the owner -> exchange path)
+    if (owner && !(a.dbg & 1)) {
+      const size_t row = (size_t)t * a.ldb + a.b0 + col;
+      a.out_aug[row * a.aug_ld + j] = hb_out;
+      a.hprev_aug[row * a.aug_ld + j] = hb_prev;
     }
     if (!exch) break;
     mbar_wait_parity(&S.bar[p], phase[p]);
@@ -325,8 +330,8 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
     __syncthreads();
     if (trace) trace[t * 4 + 3] = gtimer();
   }
-  store_step(a.T1 - 1);
   if (tid < CS) bulk_wait_read_all();
+  if (tid == STORE_TID) bulk_wait_all();  // the record stores are complete before the CTA exits
   cluster_sync_all();  // no CTA leaves while a peer may still read / write its shared memory
 }
 
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const LstmFwdAr
 __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   BwdSmem& S = *reinterpret_cast<BwdSmem*>(smraw);
-  const int H = a.H, H4 = 4 * H;
+  const int H = a.H;
   const int rank = (int)cluster_rank();
   const int cb = (blockIdx.x / CS) * NB;
   const int u0 = rank * UC;
@@ -370,24 +375,29 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
   const uint32_t ld_base = smem_u32(&S.dz[lane & 7][((lane >> 3) & 1) * 8 + (lane >> 4) * 16]);
   cluster_sync_all();
 
+  // the owner's inputs of step tt, prefetched one step ahead (issued after the previous
+  // step's owner math, so no global load sits in front of the recurrent MMAs)
+  float dho = 0.f, ig = 0.f, fg = 0.f, gg = 0.f, og = 0.f, cc = 0.f, cprev = 0.f, nd = 0.f, ndn = 0.f;
+  auto load_step = [&](int tt) {
+    if (!owner) return;
+    const size_t row = (size_t)tt * a.ldb + a.b0 + col;
+    dho = a.dh_out[row * a.dh_ld + j];
+    const float* rec = a.act8 + (row * H + j) * 8;
+    const float4 gv = *reinterpret_cast<const float4*>(rec);
+    ig = gv.x;
+    fg = gv.y;
+    gg = gv.z;
+    og = gv.w;
+    cc = rec[4];
+    nd = a.done[row] ? 0.f : 1.f;
+    cprev = tt == 0 ? a.c0[(size_t)(a.b0 + col) * H + j] : a.act8[((row - a.ldb) * H + j) * 8 + 4];
+    ndn = tt + 1 < a.T1 ? (a.done[row + a.ldb] ? 0.f : 1.f) : 0.f;
+  };
+  load_step(a.T1 - 1);
+
   for (int t = a.T1 - 1; t >= 0; --t) {
     const size_t trow = (size_t)t * a.ldb + a.b0;
     if (trace) trace[t * 4 + 0] = gtimer();
-    // the owner's inputs for this step, issued before the exchange
-    float dho = 0.f, ig = 0.f, fg = 0.f, gg = 0.f, og = 0.f, cc = 0.f, cprev = 0.f, nd = 0.f, ndn = 0.f;
-    if (owner) {
-      const size_t row = trow + col;
-      dho = a.dh_out[row * a.dh_ld + j];
-      const float* act = a.gates + row * H4;
-      ig = act[j];
-      fg = act[H + j];
-      gg = act[2 * H + j];
-      og = act[3 * H + j];
-      cc = a.cseq[row * H + j];
-      nd = a.done[row] ? 0.f : 1.f;
-      cprev = t == 0 ? a.c0[(size_t)(a.b0 + col) * H + j] : a.cseq[(row - a.ldb) * H + j];
-      if (t + 1 < a.T1) ndn = a.done[row + a.ldb] ? 0.f : 1.f;
-    }
     float dh_rec = 0.f;
     if (t + 1 < a.T1) {
       const int p = t & 1;
@@ -459,6 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
         S.dz[ob][gate * UC + ou] = zb;
         dg[gate * H + j] = zb;
       }
+      if (t > 0) load_step(t - 1);
     }
     __syncthreads();
     if (trace) trace[t * 4 + 3] = gtimer();
@@ -518,7 +529,8 @@ int lstm_cl_pack(const float* whh, int H, uint32_t* frag, cudaStream_t s) {
 static int g_cluster_ok = -1;  // -1 unknown, 0 unavailable, else max active clusters
 
 template <typename Args>
-static int cl_launch(const void* fn, const Args& a, size_t smem, const char* name, cudaStream_t s) {
+static int cl_launch(const void* fn, const Args& a, size_t smem, const char* name, cudaStream_t s,
+                     const CUtensorMap* tm = nullptr) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) {
@@ -538,7 +550,7 @@ static int cl_launch(const void* fn, const Args& a, size_t smem, const char* nam
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  void* args[] = {const_cast<Args*>(&a)};
+  void* args[] = {const_cast<Args*>(&a), const_cast<CUtensorMap*>(tm)};
   e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) {
     set_error("%s launch: %s", name, cudaGetErrorString(e));
@@ -589,7 +601,13 @@ int lstm_cl_launch_fwd(const LstmFwdArgs& a, cudaStream_t s) {
     set_error("lstm cluster: H=%d (<= %d), B pass %d (<= %d)", a.H, CS * UC, a.B, lstm_cluster_batch());
     return BP_ERR_ARG;
   }
-  return cl_launch((const void*)lstm_cl_fwd_kernel, a, sizeof(FwdSmem), "lstm_cl_fwd_kernel", s);
+  // act8 [T1][ldb][H][8] f32; one box = the CTA's UC units x the cluster's NB batch columns of a step
+  CUtensorMap tm;
+  const long long dims[4] = {8, a.H, a.ldb, a.T1};
+  const long long strides[3] = {32, 32LL * a.H, 32LL * a.H * a.ldb};
+  const int box[4] = {8, UC, NB, 1};
+  if (int e = tma_make_f32(&tm, a.act8, 4, dims, strides, box)) return e;
+  return cl_launch((const void*)lstm_cl_fwd_kernel, a, sizeof(FwdSmem), "lstm_cl_fwd_kernel", s, &tm);
 }
 
 int lstm_cl_launch_bwd(const LstmBwdArgs& a, cudaStream_t s) {

@@ -1430,7 +1430,10 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
       a.h0 = h0 + (size_t)l * B * H;
       a.c0 = c0 + (size_t)l * B * H;
       a.hx = core->hx;
-      a.gates = core->gates + (size_t)l * core->max_rows * 4 * H;
+      // per layer [max_rows][8H] f32: the cluster path's [rows][H][8] act8 records, or the
+      // cooperative path's [rows][4H] gates in its first half
+      a.gates = core->gates + (size_t)l * core->max_rows * 8 * H;
+      a.act8 = a.gates;
       a.cseq = core->cseq + (size_t)l * core->max_rows * H;
       a.out_aug = bfp(core->out, l);
       a.hprev_aug = bfp(core->hprev, l);
@@ -1518,7 +1521,8 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       a.b0 = b0;
       a.T1 = T1;
       a.whh = params + off[l ? P_WHH1 : P_WHH0];
-      a.gates = core->gates + (size_t)l * core->max_rows * 4 * H;
+      a.gates = core->gates + (size_t)l * core->max_rows * 8 * H;
+      a.act8 = a.gates;
       a.cseq = core->cseq + (size_t)l * core->max_rows * H;
       a.c0 = c0 + (size_t)l * B * H;
       a.done = done;

@@ -54,4 +54,25 @@ int tma_make_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dtype, int 
   return BP_OK;
 }
 
+int tma_make_f32(CUtensorMap* m, const void* ptr, int rank, const long long* dims, const long long* strides_b,
+                 const int* box) {
+  if (int e = tma_init()) return e;
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    bx[i] = (cuuint32_t)box[i];
+    es[i] = 1;
+    if (i + 1 < rank) st[i] = (cuuint64_t)strides_b[i];
+  }
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(ptr), d, st, bx, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32 rank %d) failed (%d)", rank, (int)r);
+    return BP_ERR_LAUNCH;
+  }
+  return BP_OK;
+}
+
 }  // namespace bp

@@ -10,4 +10,9 @@ int tma_num_sms();
 // swz in {0, 32, 64, 128} bytes.  OOB reads are zero-filled.
 int tma_make_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dtype, int esize, long long rows,
                 long long cols, int box_cols, int box_rows, int swz);
+// rank-D f32 tensor, no swizzle: dims[0] innermost (contiguous); strides_b[i] = byte stride of
+// dims[i + 1] (multiples of 16); box[] elements per dim (box[0] * 4 bytes a multiple of 16).
+// OOB elements of a store are not written.
+int tma_make_f32(CUtensorMap* m, const void* ptr, int rank, const long long* dims, const long long* strides_b,
+                 const int* box);
 }  // namespace bp

@@ -12,7 +12,7 @@ mode = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # 0 conv1, 1 conv2, 2 conv3, 3 fc, 4 heads
 keep_x0 = not (len(sys.argv) > 3 and sys.argv[3] == "nox0")
 N.lib().bp_atari_set_conv1_u8(mode)
-n = 2592
+n = int(sys.argv[4]) if len(sys.argv) > 4 else 2592
 net = AtariNet(num_actions=6)
 frames = torch.randint(0, 256, (n, 4, 84, 84), dtype=torch.uint8, device="cuda")
 rew = torch.rand(n, device="cuda")
