@@ -317,7 +317,8 @@ typedef struct BpLstmCore {
   void* dgates;   /* [N][G4] bf16 pre-activation gate gradients, zeroed once */
   float* dh;      /* [N][576] f32                                            */
   float* dx;      /* [N][576] f32                                            */
-  float* wpart;   /* [2][G4][576] f32 weight-gradient GEMM outputs           */
+  float* wpart;   /* [2][2][G4][576] f32 weight-gradient GEMM outputs (W_ih, W_hh)
+                     x (split-K halves)                                       */
 } BpLstmCore;
 size_t bp_lstm_partial_floats(int hidden);
 /* Recurrence implementation: 0 auto (16-CTA cluster kernels with W_hh in registers and

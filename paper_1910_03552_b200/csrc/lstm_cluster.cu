@@ -521,7 +521,8 @@ size_t lstm_cl_frag_words() { return (size_t)2 * CS * WARPS * ITEMS * KSMAX * 4 
 size_t lstm_cl_frag_dir_words() { return (size_t)CS * WARPS * ITEMS * KSMAX * 4 * 32; }
 
 int lstm_cl_pack(const float* whh, int H, uint32_t* frag, cudaStream_t s) {
-  lstm_cl_pack_kernel<<<296, 256, 0, s>>>(whh, H, frag);
+  // one word per thread: the per-word index math and scattered W_hh reads are latency-bound
+  lstm_cl_pack_kernel<<<(unsigned)((lstm_cl_frag_words() + 255) / 256), 256, 0, s>>>(whh, H, frag);
   return check_launch("lstm_cl_pack_kernel");
 }
 

@@ -1292,53 +1292,62 @@ extern "C" int bp_atari_backward_frames(const BpAtariNet* net, int n, const uint
 __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float* __restrict__ bih,
                                      const float* __restrict__ bhh, __nv_bfloat16* __restrict__ dst, int H,
                                      int G4) {
-  const int H4 = 4 * H;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)G4 * kCoreW;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / kCoreW), k = (int)(i % kCoreW);
-    float v = 0.f;
-    if (r < H4) v = k < H ? wih[(size_t)r * H + k] : (k == H ? bih[r] + bhh[r] : 0.f);
-    dst[i] = __float2bfloat16_rn(v);
-  }
+  // one block per output row r, one bf16 pair per thread (coalesced row reads / writes)
+  const int r = blockIdx.x, k = 2 * threadIdx.x;
+  auto val = [&](int kk) {
+    if (r >= 4 * H) return 0.f;
+    return kk < H ? wih[(size_t)r * H + kk] : (kk == H ? bih[r] + bhh[r] : 0.f);
+  };
+  reinterpret_cast<__nv_bfloat162*>(dst + (size_t)r * kCoreW)[threadIdx.x] =
+      __floats2bfloat162_rn(val(k), val(k + 1));
 }
 
 // weight-gradient GEMM outputs [G4][576] -> torch-layout grads of one layer
-__global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* __restrict__ phh,
+// (two split-K halves, `half` elements apart, summed in a fixed order)
+__global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* __restrict__ phh, size_t half,
                                     float* __restrict__ gwih, float* __restrict__ gwhh,
                                     float* __restrict__ gbih, float* __restrict__ gbhh, int H) {
-  const long long n = 4LL * H * H;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / H, k = i % H;
-    gwih[i] = pih[r * kCoreW + k];
-    gwhh[i] = phh[r * kCoreW + k];
-    if (k == 0) {
-      const float b = pih[r * kCoreW + H];
-      gbih[r] = b;
-      gbhh[r] = b;
-    }
+  // one block per gate row r, threads over the hidden columns (coalesced)
+  const int r = blockIdx.x;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) {
+    const size_t o = (size_t)r * kCoreW + k;
+    gwih[(size_t)r * H + k] = pih[o] + pih[o + half];
+    gwhh[(size_t)r * H + k] = phh[o] + phh[o + half];
+  }
+  if (threadIdx.x == 0) {
+    const size_t o = (size_t)r * kCoreW + H;
+    const float b = pih[o] + pih[o + half];
+    gbih[r] = b;
+    gbhh[r] = b;
   }
 }
 
 // d_fc [n][512] bf16 = dcore[:, :512] * relu mask; bias-gradient partials per 32-row group
-__global__ void __launch_bounds__(256) lstm_dfc_kernel(const float* __restrict__ dcore,
+__global__ void __launch_bounds__(128) lstm_dfc_kernel(const float* __restrict__ dcore,
                                                        const uint32_t* __restrict__ mc,
                                                        __nv_bfloat16* __restrict__ d_fc,
                                                        float* __restrict__ colsum, int n) {
-  const int grp = blockIdx.x;  // rows [32*grp, 32*grp + 32)
-  for (int c = threadIdx.x; c < 512; c += 256) {
-    float s = 0.f;
-    for (int i = 0; i < 32; ++i) {
-      const int m = grp * 32 + i;
-      if (m >= n) break;
-      const size_t bit = (size_t)m * kCoreW + c;
-      const float v = ((mc[bit >> 5] >> (bit & 31)) & 1u) ? dcore[(size_t)m * kCoreW + c] : 0.f;
-      const __nv_bfloat16 vb = __float2bfloat16_rn(v);
-      d_fc[(size_t)m * 512 + c] = vb;
+  // rows [32*grp, 32*grp + 32), one column per thread; the 32 loads are independent
+  const int grp = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
+  float s = 0.f;
+  const int rows = n - grp * 32 < 32 ? n - grp * 32 : 32;
+  float x[32];
+  uint32_t w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {  // every load issued before the first use
+    const size_t m = (size_t)grp * 32 + (i < rows ? i : 0), bit = m * kCoreW + c;
+    x[i] = __ldg(dcore + m * kCoreW + c);
+    w[i] = __ldg(mc + (bit >> 5)) >> (bit & 31);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < rows) {
+      const float v = (w[i] & 1u) ? x[i] : 0.f;
+      d_fc[((size_t)grp * 32 + i) * 512 + c] = __float2bfloat16_rn(v);
       s += v;
     }
-    colsum[(size_t)grp * 512 + c] = s;
   }
+  colsum[(size_t)grp * 512 + c] = s;
 }
 
 // cooperative path: recurrent partial sums; cluster path: packed W_hh fragments of both layers
@@ -1387,7 +1396,7 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
   const size_t wsz = (size_t)G4 * kCoreW;
   for (int l = 0; l < 2; ++l) {
     const int pw = l ? P_WIH1 : P_WIH0, pb = l ? P_BIH1 : P_BIH0, pc = l ? P_BHH1 : P_BHH0;
-    pack_lstm_wih_kernel<<<148, 512, 0, s>>>(params + off[pw], params + off[pb], params + off[pc], wih + l * wsz,
+    pack_lstm_wih_kernel<<<G4, kCoreW / 2, 0, s>>>(params + off[pw], params + off[pb], params + off[pc], wih + l * wsz,
                                              H, G4);
     if ((rc = check_launch("pack_lstm_wih_kernel"))) return rc;
   }
@@ -1544,13 +1553,18 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       GemmArgs g = base_args();
       g.m_tiles = G4 / 128;
       g.n_tiles = kCoreW / 64;
-      g.num_kb = g.kb_per_split = (n + 63) / 64;
+      // split-K 2 (the lstm_scatter_kernel sums the halves): 17 x 9 = 153 tiles would need a
+      // second wave for 5 tiles on 148 SMs; 306 half-K tiles fill three half-length waves
+      g.splits = 2;
+      g.num_kb = (n + 63) / 64;
+      g.kb_per_split = (g.num_kb + 1) / 2;
       g.a_atoms_per_shift = G4 / 64;
       g.a_nshifts = 1;
       g.N = kCoreW;
       g.M = G4;
       g.out_f32 = 1;
-      g.out = core->wpart + (size_t)w * G4 * kCoreW;
+      g.out = core->wpart + (size_t)w * 2 * G4 * kCoreW;
+      g.split_stride = (long long)G4 * kCoreW;
       g.r_img = kCoreW;
       if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
     }
@@ -1570,13 +1584,14 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       g.r_img = kCoreW;
       if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
     }
-    lstm_scatter_kernel<<<296, 256, 0, s>>>(core->wpart, core->wpart + (size_t)G4 * kCoreW,
+    lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)2 * G4 * kCoreW,
+                                            (size_t)G4 * kCoreW,
                                             grads + off[l ? P_WIH1 : P_WIH0], grads + off[l ? P_WHH1 : P_WHH0],
                                             grads + off[l ? P_BIH1 : P_BIH0], grads + off[l ? P_BHH1 : P_BHH0], H);
     if ((rc = check_launch("lstm_scatter_kernel"))) return rc;
   }
   // layer-0 input gradient (core->dh) -> d_fc (relu mask) + bias partials for dbfc
-  lstm_dfc_kernel<<<P.cs_rows[3], 256, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
+  lstm_dfc_kernel<<<dim3(P.cs_rows[3], 4), 128, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
                                                reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);
   if ((rc = check_launch("lstm_dfc_kernel"))) return rc;
   return torso_backward(net, n, nullptr, bfp(core->out, 1), grads, off, P, ws, s);
