@@ -242,7 +242,7 @@ int bp_atari_pack_weights(const BpAtariNet* net, const float* params, void* stre
 int bp_atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, const float* reward,
                      const int64_t* last_action, const float* params, float* logits,
                      float* baseline, void* stream);
-/* Debug: the next tcgen05 GEMM launch records per-tile role timestamps (%globaltimer, ns)
+/* Debug: the next tcgen05 GEMM launch records per-tile role timestamps (SM clock64 cycles)
  * into buf[(cta * tiles + i) * 16 + event]: 0/1 producer, 2/3 MMA, 4/5 epilogue, 6/7 u8
  * converter (start / end of tile i of that CTA), 8/9 converter loop end / fence end.  buf = null cancels. */
 int bp_gemm_trace_next(void* buf, int tiles, int skip);  /* skip: traced launch = the (skip+1)-th */
@@ -327,6 +327,9 @@ size_t bp_lstm_partial_floats(int hidden);
 int bp_lstm_set_mode(int mode);
 /* 1 if the LSTM recurrence currently runs on the cluster kernels (bf16 recurrent operands),
  * 0 if on the cooperative f32 kernels. */
+/* Diagnostics: how many 16-CTA recurrence clusters can be co-resident (8 batch columns each;
+ * 7 on a 148-SM B200, so B <= 56 runs as one pass). */
+int bp_lstm_cluster_capacity(void);
 int bp_lstm_cluster_active(void);
 /* Diagnostics: per-step %globaltimer trace of CTA 0 of the recurrent kernels into
  * buf (device u64 [2][T1][4] + 2: forward phases, backward phases, forward start /

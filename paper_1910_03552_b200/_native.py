@@ -58,6 +58,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_lstm_trace": (I, [P]),
     "bp_lstm_set_mode": (I, [I]),
     "bp_lstm_cluster_active": (I, []),
+    "bp_lstm_cluster_capacity": (I, []),
     "bp_atari_lstm_forward": (I, [P, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_forward_planes": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, P, P, P]),
     "bp_atari_lstm_backward": (I, [P, P, I, I, P, P, P, P, P, P, P]),

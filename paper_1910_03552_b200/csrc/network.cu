@@ -1363,6 +1363,7 @@ static bool lstm_use_cluster() {
 }
 
 extern "C" int bp_lstm_cluster_active(void) { return lstm_use_cluster() ? 1 : 0; }
+extern "C" int bp_lstm_cluster_capacity(void) { return lstm_cluster_batch() / 8; }
 
 static int lstm_g4(int H) { return (4 * H + 127) & ~127; }
 

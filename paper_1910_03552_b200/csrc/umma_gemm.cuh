@@ -163,10 +163,8 @@ struct GemmCfg {
   static_assert(BM == B_KMAJOR || BSWZ == 128 || (BSWZ == 64 && BN == 32), "B swizzle");
 };
 
-BP_DEVICE unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+BP_DEVICE unsigned long long gtimer() {  // SM cycle counter (per-CTA traces; %globaltimer ticks are ~1 us)
+  return (unsigned long long)clock64();
 }
 BP_DEVICE void trace_ev(const GemmArgs& g, int i, int ev) {
   if (g.trace && i < g.trace_tiles) g.trace[((size_t)blockIdx.x * g.trace_tiles + i) * 16 + ev] = gtimer();

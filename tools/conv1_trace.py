@@ -24,15 +24,14 @@ for it in range(3):
         N.lib().bp_gemm_trace_next(tr.data_ptr(), TT, skip)
     net._forward_kernels(frames, rew, la, repack=True, keep_x0=keep_x0)
 torch.cuda.synchronize()
-t = tr.view(148, TT, 16).cpu().numpy().astype(np.float64)
+t = tr.view(148, TT, 16).cpu().numpy().astype(np.float64) / 1.965  # SM cycles -> ns at 1965 MHz
 ntiles = [(n * 441 + 127) // 128, (n * 100 + 127) // 128, (n * 81 + 127) // 128,
           ((n + 127) // 128) * 8, (n + 127) // 128][skip]
 per = [len(range(b, ntiles, 148)) for b in range(148)]
-t0 = t[t > 0].min()
-t = np.where(t > 0, t - t0, np.nan)
+t = np.where(t > 0, t - t[:, :1, :1], np.nan)  # per-CTA clock origin
 print(f"== gemm #{skip} u8={mode}: tiles/CTA {per[0]}, kernel span {np.nanmax(t)/1e3:.1f} us")
 b = 0
-for i in list(range(min(per[b], 6))) + list(range(max(6, per[b] - 3), per[b])):
+for i in list(range(min(per[b], 6))) + list(range(max(6, min(per[b], TT) - 3), min(per[b], TT))):
     e = t[b, i]
     print(f"  tile {i:3d}: prod {e[0]/1e3:7.2f}-{e[1]/1e3:7.2f} conv {e[6]/1e3:7.2f}-{e[7]/1e3:7.2f} "
           f"mma {e[2]/1e3:7.2f}-{e[3]/1e3:7.2f}  epi {e[4]/1e3:7.2f}-{e[5]/1e3:7.2f} us")
