@@ -483,13 +483,20 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    # (BP_BENCH_DP_BACKEND=gloo: a test mode for the multi-rank code path on fewer GPUs than
+    # ranks -- ranks share devices round-robin, the steps are not graph-captured)
+    backend = os.environ.get("BP_BENCH_DP_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = True
 
     from paper_1910_03552_b200 import _native as N
@@ -542,6 +549,7 @@ def main():
     if launches == 0 and L._graphs:  # graph replays: every replay re-launches the captured kernels
         launches = L.kernels_per_step * args.steps
     step_s = statistics.mean(times)
+    config["cuda_graph"] = bool(L._graphs)  # False: the step ran eagerly (e.g. gloo test mode)
     if world > 1:
         t = torch.tensor([step_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

@@ -207,8 +207,21 @@ class FusedLearner:
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
                 c0 = N.lib().bp_launch_count()
-                with torch.cuda.graph(g, stream=side):
+                try:
+                    with torch.cuda.graph(g, stream=side):
+                        self._step_eager(batch, optimizer)
+                except (RuntimeError, torch.cuda.CudaError) as exc:
+                    if self.pg is None:
+                        raise
+                    # a process group whose collectives cannot be captured (NCCL without graph
+                    # support): run this learner's steps eagerly instead of failing the job
+                    torch.cuda.synchronize()
+                    self.use_graphs = False
+                    self.capture_error = repr(exc)
                     self._step_eager(batch, optimizer)
+                    if scheduler is not None:
+                        scheduler.step()
+                    return self.losses
                 self.kernels_per_step = int(N.lib().bp_launch_count() - c0)
                 torch.cuda.current_stream().wait_stream(side)
                 self._graphs[key] = g
