@@ -1331,6 +1331,10 @@ __global__ void __launch_bounds__(128) lstm_dfc_kernel(const float* __restrict__
   const int grp = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
   float s = 0.f;
   const int rows = n - grp * 32 < 32 ? n - grp * 32 : 32;
+  if (rows <= 0) {  // padding groups of the partial layout (the finalize reads their zeros)
+    colsum[(size_t)grp * 512 + c] = 0.f;
+    return;
+  }
   float x[32];
   uint32_t w[32];
 #pragma unroll
