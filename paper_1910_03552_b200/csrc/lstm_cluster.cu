@@ -33,7 +33,6 @@ constexpr int NB = 8;               // batch columns per cluster (MMA N)
 constexpr int UC = 34;              // hidden units per CTA (16 * 34 = 544 >= H)
 constexpr int RR = 4 * UC;          // 136 gate rows per CTA
 constexpr int MT = 9;               // row tiles of 16 (144 rows)
-constexpr int KPS = 552;            // h row stride (bf16): KPS/2 % 32 == 20 -> conflict-free B loads
 constexpr int KST = 34;             // K steps of 16 over 544 hidden units
 constexpr int RS = 152;             // dz row stride (bf16), RS/2 % 32 == 12
 constexpr int WARPS = 12;
@@ -58,6 +57,15 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 // four 8x8 bf16 matrices; lane l supplies the row address of matrix l/8, row l%8
 __device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// four transposed 8x8 bf16 matrices (B operand stored [k][n]); lane l supplies the address of
+// row l % 8 of matrix l / 8
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                                  uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
@@ -98,17 +106,18 @@ __device__ unsigned long long* g_cl_trace = nullptr;  // diagnostics (bp_lstm_tr
 // SM cycle counter (one SM records: consistent; %globaltimer is too coarse for sub-us phases)
 __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
 
-constexpr int SL = 40;              // padded slice width (units) of one CTA: 80 B rows
-constexpr uint32_t FWD_SLICE = NB * SL * 2;           // bytes of one CTA's h slice
+constexpr int KH = CS * UC;         // 544 hidden rows of the transposed recurrent operand
+constexpr uint32_t FWD_SLICE = UC * NB * 2;           // bytes of one CTA's h slice ([unit][batch])
 constexpr uint32_t BWD_SLICE = UC * NB * 4;           // bytes of one CTA's partial for one owner
 constexpr int OWNERS = UC * NB;                       // 272 owner threads (warps 0..8)
 
 struct FwdSmem {
   float rec[2][NB][UC][8];               // step records {i, f, g, o, c, -} by step parity: the
                                          // box of one 4D TMA store (act8, [rows][H][8])
-  __nv_bfloat16 h[NB][KPS];              // MMA operand h_{t-1}: [batch][unit]
-  __nv_bfloat16 in[2][CS][NB][SL];       // incoming slices: [parity][source CTA][batch][unit]
-  __nv_bfloat16 out[NB][SL];             // this CTA's new h slice
+  __nv_bfloat16 hT[2][KH][NB];           // MMA operand h_{t-1}, transposed [unit][batch], by step
+                                         // parity: every CTA's slice lands here directly (one
+                                         // contiguous 544 B block per source), no unpack
+  __nv_bfloat16 out[UC][NB];             // this CTA's new h slice [unit][batch]
   float red[4][MT * 16][NB];             // per K-quarter partial pre-gates
   uint64_t bar[2];                       // incoming-slice barriers, by step parity
 };
@@ -176,14 +185,14 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
         for (int r = 0; r < 4; ++r) af[s][q][r] = __ldg(fp + ((s * KSMAX + q) * 4 + r) * 32);
   }
   // ---- h0 of this cluster's columns (all units); padding zero
-  for (int i = tid; i < NB * KPS; i += THREADS) {
-    const int b = i / KPS, k = i % KPS;
+  for (int i = tid; i < KH * NB; i += THREADS) {
+    const int k = i / NB, b = i % NB;
     const int col = cb + b;
     float v = 0.f;
     if (k < H && col < a.B) v = a.h0[(size_t)(a.b0 + col) * H + k];
-    S.h[b][k] = __float2bfloat16_rn(v);
+    S.hT[0][k][b] = __float2bfloat16_rn(v);
   }
-  for (int i = tid; i < NB * SL; i += THREADS) (&S.out[0][0])[i] = __float2bfloat16_rn(0.f);
+  for (int i = tid; i < UC * NB; i += THREADS) (&S.out[0][0])[i] = __float2bfloat16_rn(0.f);
   if (tid == 0) {
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
@@ -206,10 +215,9 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
     donen = a.done[row];
   }
   uint32_t phase[2] = {0u, 0u};
-  // ldmatrix row address: matrix m = lane / 8 -> (k-step +m/2, k half m%2), row n = lane % 8
-  const uint32_t ld_base = smem_u32(&S.h[lane & 7][((lane >> 3) & 1) * 8 + (lane >> 4) * 16]);
-  // unpack role: (batch, unit pair) fixed per thread, loop over the 16 sources
-  const int ub = tid / (UC / 2), uw = tid % (UC / 2);
+  // ldmatrix.trans row address: lane l -> hidden row 16 ks + l (matrices: k-step ks rows 0-7,
+  // 8-15, k-step ks + 1 rows 0-7, 8-15), 16 B per row
+  const uint32_t ld_base = smem_u32(&S.hT[0][lane][0]);
   const int ncols = a.B - cb < NB ? a.B - cb : NB;
   cluster_sync_all();  // every CTA running, barriers initialised, before any DSMEM traffic
   if (trace) trace[4 * a.T1 * 2 + 1] = gtimer();
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
           const int ks = kq * 9 + q;
           if (ks < KST && !(a.dbg & 2)) {
             uint32_t b0, b1, b2, b3;  // k-steps ks and ks + 1
-            ldmatrix_x4(ld_base + (uint32_t)ks * 32u, b0, b1, b2, b3);
+            ldmatrix_x4_trans(ld_base + (uint32_t)((t & 1) * KH * NB * 2 + ks * 256), b0, b1, b2, b3);
             mma16816(acc[s], af[s][q], b0, b1);
             if (q + 1 < KSMAX && ks + 1 < KST) mma16816(acc[s], af[s][q + 1], b2, b3);
           }
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
       c = fg * (nd * c) + ig * gg;
       const float h = og * tanh_fast(c);
       const __nv_bfloat16 hb = __float2bfloat16_rn(h);
-      S.out[ob][ou] = hb;
+      S.out[ou][ob] = hb;
       if (!(a.dbg & 1)) {
         *reinterpret_cast<float4*>(&S.rec[p][ob][ou][0]) = make_float4(ig, fg, gg, og);
         S.rec[p][ob][ou][4] = c;
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
       if (lane == 0) mbar_expect_tx(&S.bar[p], CS * FWD_SLICE);
       if (lane < CS) {
         fence_proxy_async_smem();
-        bulk_s2cluster(mapa(smem_u32(&S.in[p][rank][0][0]), (uint32_t)lane), smem_u32(&S.out[0][0]),
+        bulk_s2cluster(mapa(smem_u32(&S.hT[(t + 1) & 1][rank * UC][0]), (uint32_t)lane), smem_u32(&S.out[0][0]),
                        FWD_SLICE, mapa(smem_u32(&S.bar[p]), (uint32_t)lane));
         bulk_commit();
       }
@@ -317,17 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
     if (!exch) break;
     mbar_wait_parity(&S.bar[p], phase[p]);
     phase[p] ^= 1u;
-    // ---- unpack the 16 slices into the MMA operand (u32 = 2 units)
-    if (tid < NB * (UC / 2)) {
-      const uint32_t* srcp = reinterpret_cast<const uint32_t*>(&S.in[p][0][ub][2 * uw]);
-      uint32_t* dstp = reinterpret_cast<uint32_t*>(&S.h[ub][2 * uw]);
-      uint32_t v[CS];
-#pragma unroll
-      for (int src = 0; src < CS; ++src) v[src] = srcp[src * (FWD_SLICE / 4)];
-#pragma unroll
-      for (int src = 0; src < CS; ++src) dstp[src * (UC / 2)] = v[src];
-    }
-    __syncthreads();
+    // (the slices landed in hT[(t + 1) & 1]: each thread's own wait orders its reads of them;
+    //  S.red / S.out / S.rec reuse is ordered by the barriers of the next step)
     if (trace) trace[t * 4 + 3] = gtimer();
   }
   if (tid < CS) bulk_wait_read_all();
