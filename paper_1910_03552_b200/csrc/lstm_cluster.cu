@@ -124,7 +124,7 @@ struct FwdSmem {
 
 struct BwdSmem {
   float recv[2][CS][UC][NB];             // [parity][source CTA][unit][batch] partial W^T dz
-  float part[CS][UC][NB];                // outgoing partials, by owner CTA
+  float part[2][CS][UC][NB];             // outgoing partials, by step parity and owner CTA
   __nv_bfloat16 dz[NB][RS];              // own dz, [batch][local gate row]
   uint64_t bar[2];
 };
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
   unsigned long long* trace = (blockIdx.x == 0 && tid == 0) ? g_cl_trace : nullptr;
   if (trace) trace += (size_t)4 * a.T1;
   for (int i = tid; i < NB * RS; i += THREADS) (&S.dz[0][0])[i] = __float2bfloat16_rn(0.f);
-  for (int i = tid; i < CS * UC * NB; i += THREADS) (&S.part[0][0][0])[i] = 0.f;
+  for (int i = tid; i < 2 * CS * UC * NB; i += THREADS) (&S.part[0][0][0][0])[i] = 0.f;
   if (tid == 0) {
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
@@ -417,8 +417,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
             }
           }
         }
-        if (tid < CS) bulk_wait_read_all();  // the previous step's copies have read S.part
-        __syncthreads();
+        // (S.part[p] was last read by the copies of step t + 2: waited for at the end of t + 1)
 #pragma unroll
         for (int s = 0; s < ITEMS; ++s) {
           const int mt = warp + WARPS * s;
@@ -427,7 +426,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
             for (int half = 0; half < 2; ++half) {
               const int jj = mt * 16 + g + 8 * half;
               if (jj < H)
-                *reinterpret_cast<float2*>(&S.part[jj / UC][jj % UC][2 * tig]) =
+                *reinterpret_cast<float2*>(&S.part[p][jj / UC][jj % UC][2 * tig]) =
                     make_float2(acc[s][2 * half], acc[s][2 * half + 1]);
             }
           }
@@ -439,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
         if (lane == 0) mbar_expect_tx(&S.bar[p], CS * BWD_SLICE);
         if (lane < CS) {
           fence_proxy_async_smem();
-          bulk_s2cluster(mapa(smem_u32(&S.recv[p][rank][0][0]), (uint32_t)lane), smem_u32(&S.part[lane][0][0]),
+          bulk_s2cluster(mapa(smem_u32(&S.recv[p][rank][0][0]), (uint32_t)lane), smem_u32(&S.part[p][lane][0][0]),
                          BWD_SLICE, mapa(smem_u32(&S.bar[p]), (uint32_t)lane));
           bulk_commit();
         }
@@ -470,6 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
       }
       if (t > 0) load_step(t - 1);
     }
+    if (tid < CS) bulk_wait_read_1();  // step t+1's copies have read S.part[p ^ 1] (reused by t - 1)
     __syncthreads();
     if (trace) trace[t * 4 + 3] = gtimer();
   }
