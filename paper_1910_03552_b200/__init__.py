@@ -7,6 +7,7 @@ Hot path, all sm_100a CUDA behind the C ABI in include/beast_b200.h:
   optim         fused global-norm clip + RMSProp
   atari_net     AtariNet (conv torso + FC [+ LSTM] + heads) on tcgen05
   learner       learn() -- the whole step, optionally data-parallel over B
+  inference     ActorInference -- the actor-inference loop body (fused Gumbel-max sampling)
 """
 from .errors import DimensionError, NativeError, NonFiniteError, SchemaError  # noqa: F401
 
