@@ -863,6 +863,7 @@ static int heads_forward(const BpAtariNet* net, int n, const void* head_in, floa
     g.sample_seed = smp->seed;
     g.seed_state = smp->seed_state;
     g.greedy = smp->greedy;
+    return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 0, 0, EPK_HEADS>(g, ta, tb, s);
   }
   return launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true>(g, ta, tb, s);
 }

@@ -255,7 +255,10 @@ BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 //   EPK_GEN   every feature from GemmArgs at run time (f32 partials, heads, tests);
 //   EPK_FWD   conv / fc forward: alpha * acc + bias, ReLU, relu bits (when bits_out), bf16 out;
 //   EPK_DGRAD data gradient: relu-backward mask, bf16 out, optional column sums.
-enum { EPK_GEN = 0, EPK_FWD = 1, EPK_DGRAD = 2 };
+//   EPK_HEADS the heads forward with the fused action sampler (inference only: the Philox code
+//             stays out of the EPK_GEN instantiations, where it cost the heads / fc gradient
+//             GEMMs 13 us per learner step in code size and registers).
+enum { EPK_GEN = 0, EPK_FWD = 1, EPK_DGRAD = 2, EPK_HEADS = 3 };
 
 // element offset of column n (the column map; n is warp-uniform)
 BP_DEVICE long long col_offset(const GemmArgs& g, int n) {
@@ -275,7 +278,7 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
   if (n0 >= g.N) return;  // a partial last column tile (warp-uniform)
   const bool row_ok = roff >= 0;
   constexpr bool GEN = EK == EPK_GEN;
-  if (GEN && g.heads) {
+  if ((GEN || EK == EPK_HEADS) && g.heads) {
     if (row_ok) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {  // compile-time indices keep v[] in registers
@@ -283,7 +286,11 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
         else if (n0 + j == g.A) g.baseline[m] = v[j];
       }
       // fused sampling: the whole row (A + 1 <= 32 columns) is in this thread's registers
-      if (g.actions && n0 == 0) g.actions[m] = gumbel_argmax<32>(v, g.A, g.seed_state ? *g.seed_state : g.sample_seed, (unsigned long long)m, g.greedy != 0);
+      if constexpr (EK == EPK_HEADS) {
+        if (g.actions && n0 == 0)
+          g.actions[m] = gumbel_argmax<32>(v, g.A, g.seed_state ? *g.seed_state : g.sample_seed,
+                                           (unsigned long long)m, g.greedy != 0);
+      }
     }
     return;
   }
