@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwd
     hown = a.h0[(size_t)(a.b0 + ob) * H + j];
     const size_t row = (size_t)a.b0 + ob;
 #pragma unroll
-    for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[row * a.gx_ld + gate * H + j];
+    for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[row * a.gx_ld + j * 4 + gate];
     donen = a.done[row];
   }
   const int rg = lane >> 3, bg = lane & 7;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_fwd_kernel(const LstmFwd
       if (t + 1 < a.T1) {  // next step's inputs
         const size_t nrow = row + a.ldb;
 #pragma unroll
-        for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[nrow * a.gx_ld + gate * H + j];
+        for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[nrow * a.gx_ld + j * 4 + gate];
         donen = a.done[nrow];
       }
       a.hprev_aug[row * a.aug_ld + j] = __float2bfloat16_rn(nd * hown);
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(const LstmBwd
 #pragma unroll
       for (int gate = 0; gate < 4; ++gate) {
         zs[(gate * kLstmU + ou) * kLstmB + ob] = dz[gate];
-        dg[gate * H + j] = __float2bfloat16_rn(dz[gate]);
+        dg[j * 4 + gate] = __float2bfloat16_rn(dz[gate]);
       }
     }
     __syncthreads();

@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
     c = a.c0[row * H + j];
     hown = a.h0[row * H + j];
 #pragma unroll
-    for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[row * a.gx_ld + gate * H + j];
+    {  // gate-interleaved gx columns (j * 4 + gate): one 16-byte load
+      const float4 v = *reinterpret_cast<const float4*>(a.gx + row * a.gx_ld + (size_t)j * 4);
+      gxn[0] = v.x; gxn[1] = v.y; gxn[2] = v.z; gxn[3] = v.w;
+    }
     donen = a.done[row];
   }
   uint32_t phase[2] = {0u, 0u};
@@ -270,12 +273,6 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
         const int R = gate * UC + ou;
         z[gate] = nd * ((S.red[0][R][ob] + S.red[1][R][ob]) + (S.red[2][R][ob] + S.red[3][R][ob])) + gxn[gate];
       }
-      if (t + 1 < a.T1) {
-        const size_t nrow = row + a.ldb;
-#pragma unroll
-        for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[nrow * a.gx_ld + gate * H + j];
-        donen = a.done[nrow];
-      }
       const float ig = sigm(z[0]), fg = sigm(z[1]), gg = tanh_fast(z[2]), og = sigm(z[3]);
       c = fg * (nd * c) + ig * gg;
       const float h = og * tanh_fast(c);
@@ -316,11 +313,21 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
         bulk_commit();
       }
     }
-    // the bf16 sequences: stored while the slices travel (off the owner -> exchange path)
-    if (owner && !(a.dbg & 1)) {
+    // the bf16 sequences: stored while the slices travel (off the owner -> exchange path);
+    // the next step's inputs are prefetched here too -- issued before the owners' proxy fence
+    // (MEMBAR) they would have stalled it until they returned
+    if (owner) {
       const size_t row = (size_t)t * a.ldb + a.b0 + col;
-      a.out_aug[row * a.aug_ld + j] = hb_out;
-      a.hprev_aug[row * a.aug_ld + j] = hb_prev;
+      if (!(a.dbg & 1)) {
+        a.out_aug[row * a.aug_ld + j] = hb_out;
+        a.hprev_aug[row * a.aug_ld + j] = hb_prev;
+      }
+      if (t + 1 < a.T1) {
+        const size_t nrow = row + a.ldb;
+#pragma unroll
+        for (int gate = 0; gate < 4; ++gate) gxn[gate] = a.gx[nrow * a.gx_ld + (size_t)j * 4 + gate];
+        donen = a.done[nrow];
+      }
     }
     if (!exch) break;
     mbar_wait_parity(&S.bar[p], phase[p]);
@@ -460,13 +467,17 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
       const float dz[4] = {dc * gg * ig * (1.f - ig), dc * cprev * fg * (1.f - fg), dc * ig * (1.f - gg * gg),
                            dh * tc * og * (1.f - og)};
       dcf = dc * fg;
-      __nv_bfloat16* dg = a.dgates + row * a.dg_ld;
+      // gate-interleaved dgates columns (j * 4 + gate): one 8-byte store
+      uint32_t zp[2];
 #pragma unroll
       for (int gate = 0; gate < 4; ++gate) {
         const __nv_bfloat16 zb = __float2bfloat16_rn(dz[gate]);
         S.dz[ob][gate * UC + ou] = zb;
-        dg[gate * H + j] = zb;
+        const uint32_t bits = __bfloat16_as_ushort(zb);
+        if (gate & 1) zp[gate >> 1] |= bits << 16;
+        else zp[gate >> 1] = bits;
       }
+      *reinterpret_cast<uint2*>(a.dgates + row * a.dg_ld + (size_t)j * 4) = make_uint2(zp[0], zp[1]);
       if (t > 0) load_step(t - 1);
     }
     if (tid < CS) bulk_wait_read_1();  // step t+1's copies have read S.part[p ^ 1] (reused by t - 1)

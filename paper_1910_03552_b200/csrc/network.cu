@@ -1293,13 +1293,16 @@ extern "C" int bp_atari_backward_frames(const BpAtariNet* net, int n, const uint
 __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float* __restrict__ bih,
                                      const float* __restrict__ bhh, __nv_bfloat16* __restrict__ dst, int H,
                                      int G4) {
-  // one block per output row r, one bf16 pair per thread (coalesced row reads / writes)
-  const int r = blockIdx.x, k = 2 * threadIdx.x;
+  // one block per output row, one bf16 pair per thread (coalesced row reads / writes).
+  // Output row rp = j * 4 + gate holds torch row r = gate * H + j: the gate-interleaved G4
+  // order of gx, dgates and the weight-gradient rows (an owner's 4 gates are contiguous)
+  const int rp = blockIdx.x, k = 2 * threadIdx.x;
+  const int r = rp < 4 * H ? (rp & 3) * H + (rp >> 2) : 4 * H;
   auto val = [&](int kk) {
     if (r >= 4 * H) return 0.f;
     return kk < H ? wih[(size_t)r * H + kk] : (kk == H ? bih[r] + bhh[r] : 0.f);
   };
-  reinterpret_cast<__nv_bfloat162*>(dst + (size_t)r * kCoreW)[threadIdx.x] =
+  reinterpret_cast<__nv_bfloat162*>(dst + (size_t)rp * kCoreW)[threadIdx.x] =
       __floats2bfloat162_rn(val(k), val(k + 1));
 }
 
@@ -1308,15 +1311,17 @@ __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float*
 __global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* __restrict__ phh, size_t half,
                                     float* __restrict__ gwih, float* __restrict__ gwhh,
                                     float* __restrict__ gbih, float* __restrict__ gbhh, int H) {
-  // one block per gate row r, threads over the hidden columns (coalesced)
+  // one block per torch gate row r (= GEMM row rp = j * 4 + gate, gate-interleaved order),
+  // threads over the hidden columns (coalesced)
   const int r = blockIdx.x;
+  const int rp = (r % H) * 4 + r / H;
   for (int k = threadIdx.x; k < H; k += blockDim.x) {
-    const size_t o = (size_t)r * kCoreW + k;
+    const size_t o = (size_t)rp * kCoreW + k;
     gwih[(size_t)r * H + k] = pih[o] + pih[o + half];
     gwhh[(size_t)r * H + k] = phh[o] + phh[o + half];
   }
   if (threadIdx.x == 0) {
-    const size_t o = (size_t)r * kCoreW + H;
+    const size_t o = (size_t)rp * kCoreW + H;
     const float b = pih[o] + pih[o + half];
     gbih[r] = b;
     gbhh[r] = b;
