@@ -381,11 +381,17 @@ int bp_infeed_get(void* stream, void* release_event, void* ready_event);
 /* Learner-step stats read-back (monobeast learn() stats: losses + episode returns of the
  * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
  * (nullable) and the status word (nullable; read, then cleared for the next step) into
- * out = [32 B losses | 4 B status | 4 B pad | tb B done | tb * 4 B returns] in one launch.
+ * out = [32 B losses | 4 B status | 4 B seq | tb B done | tb * 4 B returns] in one launch.
  * out may be device memory or pinned host memory (written through its unified-address
- * mapping: the step's result reaches the host without a separate copy). */
+ * mapping: the step's result reaches the host without a separate copy).  seq_state
+ * (nullable; 2 x u32 device memory, zeroed once) makes the pack publish a completion
+ * sequence number in the seq word (1, 2, ... per call) after all its other writes are visible
+ * system-wide: the host can spin on it instead of synchronising on an event. */
 int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                  unsigned* status, void* out, void* stream);
+                  unsigned* status, unsigned* seq_state, void* out, void* stream);
+/* Host-side wait for a completion word in pinned host memory, e.g. the seq word of
+ * bp_pack_stats: returns 0 once (*word - want) mod 2^32 < 2^31, 1 after timeout_us. */
+int bp_host_wait_seq(const unsigned* word, unsigned want, long long timeout_us);
 /* Shifted-tap GEMM test entry (the convolution form of the engine):
  * C[m][n] = sum_t sum_c A[m + offs[t]][c] * B[n][t*Cin + c]; window_mode 0 = one TMA box
  * per tap, 1 / 2 = one shared window per channel block (descriptor base offset 0 / row&7).

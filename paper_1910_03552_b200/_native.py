@@ -66,7 +66,8 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_forward_sample": (I, [P, I, P, P, I, P, P, P, C.c_uint64, P, I, P, P, P, P]),
     "bp_atari_lstm_forward_sample": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, C.c_uint64, P, I,
                                          P, P, P, P, P, P]),
-    "bp_pack_stats": (I, [P, P, P, I, P, P, P]),
+    "bp_pack_stats": (I, [P, P, P, I, P, P, P, P]),
+    "bp_host_wait_seq": (I, [P, C.c_uint, C.c_longlong]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),
     "bp_infeed_get": (I, [P, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),

@@ -1,5 +1,7 @@
 // C-ABI glue: version, thread-local error message, launch checking.
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -41,3 +43,24 @@ bool pdl_enabled() {
 extern "C" int bp_abi_version(void) { return 1; }
 extern "C" const char* bp_last_error(void) { return bp::g_err; }
 extern "C" unsigned long long bp_launch_count(void) { return bp::g_launches.load(); }
+
+// Host-side wait on a completion word in pinned memory (a device kernel publishes it through the
+// unified-address mapping, e.g. bp_pack_stats' seq word): spins until (*word - want) mod 2^32 is
+// below 2^31, yielding the core every 1024 polls.  Called through ctypes it runs without the
+// Python GIL.  Returns 0 when reached, 1 after timeout_us.
+extern "C" int bp_host_wait_seq(const unsigned* word, unsigned want, long long timeout_us) {
+  const volatile unsigned* w = word;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned long long i = 0;; ++i) {
+    if ((unsigned)(*w - want) < 0x80000000u) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return 0;
+    }
+    if ((i & 1023) == 1023) {
+      if (std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >
+          timeout_us)
+        return 1;
+      std::this_thread::yield();
+    }
+  }
+}

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
                                                          const uint8_t* __restrict__ done,
                                                          const float* __restrict__ ret, int tb,
                                                          unsigned* __restrict__ status,
+                                                         unsigned* __restrict__ seq_state,
                                                          uint8_t* __restrict__ out) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -171,11 +172,10 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
       *status = 0u;
     }
     reinterpret_cast<unsigned*>(out)[8] = st;
-    reinterpret_cast<unsigned*>(out)[9] = 0u;
   }
-  if (i >= tb) return;
-  out[kStatsHead + i] = done[i] ? 1 : 0;
-  if (ret) {
+  if (i < tb) {
+    out[kStatsHead + i] = done[i] ? 1 : 0;
+    if (ret) {
     uint8_t* o = out + kStatsHead + tb;
     if ((tb & 3) == 0) {
       reinterpret_cast<float*>(o)[i] = ret[i];
@@ -186,9 +186,22 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
       o[4 * i + 2] = (uint8_t)(v >> 16);
       o[4 * i + 3] = (uint8_t)(v >> 24);
     }
+    }
   }
-  // (out may be mapped pinned host memory: the host reads it after an event synchronize on
-  // the stream, which orders these writes)
+  // completion word (seq_state != null): the last block to finish publishes the pack's
+  // sequence number in word 9 after every block's writes are visible system-wide, so a host
+  // thread can spin on the pinned buffer instead of synchronising on an event
+  if (seq_state) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&seq_state[0], 1u) == gridDim.x - 1) {
+      seq_state[0] = 0u;
+      const unsigned s = seq_state[1] + 1u;
+      seq_state[1] = s;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(out + 36) = s;
+    }
+  }
 }
 
 }  // namespace bp
@@ -196,14 +209,14 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
 using namespace bp;
 
 extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                             unsigned* status, void* out, void* stream) {
+                             unsigned* status, unsigned* seq_state, void* out, void* stream) {
   if (!losses || !done || !out || tb < 0) {
     set_error("pack_stats: bad args");
     return BP_ERR_ARG;
   }
   const int n = tb > 5 ? tb : 5;
   launch_pdl(pack_stats_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, losses, done,
-             episode_return, tb, status, reinterpret_cast<uint8_t*>(out));
+             episode_return, tb, status, seq_state, reinterpret_cast<uint8_t*>(out));
   return check_launch("pack_stats_kernel");
 }
 

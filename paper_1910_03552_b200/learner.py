@@ -80,6 +80,14 @@ class FusedLearner:
         hnp = self._stats_host.numpy()
         self._np_losses = hnp[:32].view(np.float64)
         self._np_status = hnp[32:36].view(np.uint32)
+        # completion sequence number, published by the pack kernel after its other writes
+        # (bp_pack_stats seq_state): stats() spins on it instead of an event round trip
+        self._np_seq = hnp[36:40].view(np.uint32)
+        self._np_seq[0] = 0
+        self._seq_state = torch.zeros(2, dtype=torch.int32, device=dev)
+        self._packs = 0  # packs enqueued (graph replays included)
+        self._seq_addr = self._stats_host.data_ptr() + 36
+        self._c_wait = N.lib().bp_host_wait_seq
         self._np_done = hnp[40:40 + tb].view(np.bool_)
         self._np_ret = hnp[40 + tb:].view(np.float32)
         # this learner's device status word: the fused loss ORs violation bits into it, the
@@ -103,6 +111,7 @@ class FusedLearner:
         self._graphs: collections.OrderedDict = collections.OrderedDict()  # LRU, <= MAX_GRAPHS
         self._seen: collections.OrderedDict = collections.OrderedDict()
         self._validated: set = set()  # graph keys whose batch schema was checked
+        self._key_memo: dict = {}     # id(batch) -> (tensors, versions, addresses, optimiser, gen, key, batch)
         self._buf_gen = model.buffer_generation
         # data parallel: the fc weight gradient (95% of the no-LSTM parameters) is all-reduced on
         # a side stream as soon as the backward has written it (BpAtariNet.fc_grad_ready), while
@@ -128,11 +137,24 @@ class FusedLearner:
 
     def _graph_key(self, batch, optimizer):
         """A captured step reads raw device addresses: key it on every batch tensor's address,
-        dtype, shape and strides, the optimiser, and the model's activation-buffer generation."""
+        dtype, shape and strides, the optimiser, and the model's activation-buffer generation.
+        Memoised per batch dict (e.g. the DeviceInfeed slots): a hit needs the same tensor
+        objects (held by the memo, so their ids cannot be recycled) at the same version counters
+        and addresses -- in-place reshapes / set_() bump the version or move the data."""
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
         ts = [batch[k] for k in self._fields(batch)] + ([ep] if ep is not None else [])
-        return tuple((t.data_ptr(), t.dtype, tuple(t.shape), t.stride()) for t in ts) + (
+        m = self._key_memo.get(id(batch))
+        if (m is not None and m[3] is optimizer and m[4] == self.model.buffer_generation and len(m[0]) == len(ts)
+                and all(a is b and a._version == v and a.data_ptr() == p
+                        for a, b, v, p in zip(ts, m[0], m[1], m[2]))):
+            return m[5]
+        key = tuple((t.data_ptr(), t.dtype, tuple(t.shape), t.stride()) for t in ts) + (
             ep is not None, id(optimizer), self.model.buffer_generation)
+        self._key_memo[id(batch)] = (tuple(ts), tuple(t._version for t in ts), tuple(t.data_ptr() for t in ts),
+                                     optimizer, self.model.buffer_generation, key, batch)
+        while len(self._key_memo) > 2 * MAX_GRAPHS:
+            self._key_memo.pop(next(iter(self._key_memo)))
+        return key
 
     def validate(self, batch):
         """Host-side schema checks of validate_batch (rollout.py:160-192): shapes and dtypes
@@ -164,6 +186,7 @@ class FusedLearner:
 
     def _drop_graphs(self):
         self._graphs.clear()
+        self._key_memo.clear()
         self._seen.clear()
         self._validated.clear()
 
@@ -234,6 +257,7 @@ class FusedLearner:
                 if self.model.mirror_stale():  # e.g. load_state_dict between steps
                     self.model.pack_weights()
                 g.replay()
+                self._packs += 1  # the replayed step packs its stats
                 if scheduler is not None:
                     scheduler.step()
                 return self.losses
@@ -341,17 +365,35 @@ class FusedLearner:
             if ep.dtype != torch.float32 or not ep.is_contiguous():
                 ep = ep.float().contiguous()
         losses = losses if losses.dtype == torch.float64 and losses.is_contiguous() else losses.double().contiguous()
+        if not torch.cuda.is_current_stream_capturing():  # (a capture runs nothing; replays count)
+            self._packs += 1
         N.check(N.lib().bp_pack_stats(losses.data_ptr(), done.data_ptr(), ep.data_ptr() if ep is not None else None,
-                                      tb, self.status.ptr(), host.data_ptr(), N.stream_handle(losses.device)),
+                                      tb, self.status.ptr(), self._seq_state.data_ptr(), host.data_ptr(),
+                                      N.stream_handle(losses.device)),
                 "bp_pack_stats")
+
+    def _wait_pack(self):
+        """Wait for the latest enqueued stats pack: spin on its completion word in the pinned
+        buffer (sub-microsecond wake-up, no driver call); after ~50 ms of spinning fall back to
+        a stream synchronise, which also surfaces device errors."""
+        want = self._packs & 0xFFFFFFFF
+        flag = self._np_seq
+        # done once the published sequence number reached `want` (wrap-around safe; packs
+        # replayed outside step() only move it further ahead)
+        if ((int(flag[0]) - want) & 0xFFFFFFFF) < 0x80000000:
+            return
+        # the spin runs in C without the GIL (other Python threads keep running)
+        if self._c_wait(self._seq_addr, want, 50_000):
+            torch.cuda.current_stream(self.model.flat_params.device).synchronize()
+            if ((int(flag[0]) - want) & 0xFFFFFFFF) >= 0x80000000:
+                raise RuntimeError(f"learner stats pack {want} never completed (seq {int(flag[0])})")
 
     def stats(self, batch, losses=None):
         """Upstream learn() stats dict from the step's packed read-back (one sync)."""
         if losses is not None:  # an explicit loss vector: pack it now
             self._pack_stats(batch, losses)
         ep = batch.get("episode_return") if isinstance(batch, dict) else None
-        self._stats_event.record()
-        self._stats_event.synchronize()
+        self._wait_pack()
         bits = int(self._np_status[0])
         pg, base, ent, total = self._np_losses.tolist()
         if bits or not np.isfinite(total):
