@@ -280,15 +280,25 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
     }
     return;
   }
+  // core columns [512, 576) of row img: 8 threads per row, one 16-byte store of 8 bf16 each
   const long long i = (long long)(blockIdx.x - 36) * blockDim.x + threadIdx.x;
-  if (i >= (long long)n * 64) return;
-  const long long img = i >> 6;
-  const int j = (int)(i & 63);
-  float v = 0.f;
-  if (j == 0) v = fminf(fmaxf(reward[img], -1.f), 1.f);
-  else if (j <= A) v = (last_action[img] == j - 1) ? 1.f : 0.f;
-  else if (j == A + 1) v = 1.f;
-  core[img * kCoreW + 512 + j] = __float2bfloat16_rn(v);
+  if (i >= (long long)n * 8) return;
+  const long long img = i >> 3;
+  const int j0 = (int)(i & 7) * 8;
+  const float r = fminf(fmaxf(reward[img], -1.f), 1.f);
+  const long long la = last_action[img];
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float v2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + 2 * q + h;
+      v2[h] = j == 0 ? r : j <= A ? (la == j - 1 ? 1.f : 0.f) : (j == A + 1 ? 1.f : 0.f);
+    }
+    w[q] = pack_bf16x2(v2[0], v2[1]);
+  }
+  *reinterpret_cast<uint4*>(core + img * kCoreW + 512 + j0) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // G [N][64] bf16 = [d_logits (A) | d_baseline | 0 ...]
@@ -694,7 +704,7 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
   if (conv1_u8()) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
-    launch_pdl(prep_kernel, dim3(36 + (n * 64 + 511) / 512), dim3(512), 0, s, params + off[P_WP],
+    launch_pdl(prep_kernel, dim3(36 + (n * 8 + 511) / 512), dim3(512), 0, s, params + off[P_WP],
                params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf), reward, last_action,
                bf(net->core), n, A);
     if ((rc = check_launch("prep_kernel"))) return rc;
@@ -959,6 +969,7 @@ static int heads_backward(const BpAtariNet* net, int n, const float* d_logits, c
     g.out = net->d_fc;
     g.r_img = 512;
     g.colsum = ws + P.cs_off[3];
+    return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_DGRAD>(g, ta, tb, s);
   }
   return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
 }

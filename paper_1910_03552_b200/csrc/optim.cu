@@ -156,16 +156,16 @@ __global__ void __launch_bounds__(kOptThreads)
 // stats read-back buffer: [losses 4 x f64 | status u32 | pad u32 | done tb x u8 | returns tb x f32
 // at byte offset 40 + tb (byte stores when that is not 4-byte aligned)]; one element per thread
 constexpr int kStatsHead = 40;
-__global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restrict__ losses,
+__global__ void __launch_bounds__(1024) pack_stats_kernel(const double* __restrict__ losses,
                                                          const uint8_t* __restrict__ done,
                                                          const float* __restrict__ ret, int tb,
                                                          unsigned* __restrict__ status,
                                                          unsigned* __restrict__ seq_state,
                                                          uint8_t* __restrict__ out) {
   pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < 4) reinterpret_cast<double*>(out)[i] = losses[i];
-  if (i == 4) {  // the step's status word: read back, then cleared for the next step
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i0 < 4) reinterpret_cast<double*>(out)[i0] = losses[i0];
+  if (i0 == 4) {  // the step's status word: read back, then cleared for the next step
     unsigned st = 0u;
     if (status) {
       st = *status;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) pack_stats_kernel(const double* __restric
     }
     reinterpret_cast<unsigned*>(out)[8] = st;
   }
-  if (i < tb) {
+  for (int i = i0; i < tb; i += gridDim.x * blockDim.x) {  // (few blocks: one system fence each)
     out[kStatsHead + i] = done[i] ? 1 : 0;
     if (ret) {
     uint8_t* o = out + kStatsHead + tb;
@@ -215,7 +215,8 @@ extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const fl
     return BP_ERR_ARG;
   }
   const int n = tb > 5 ? tb : 5;
-  launch_pdl(pack_stats_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, losses, done,
+  const int blocks = (n + 8191) / 8192;  // 1024 threads x <= 8 elements per block
+  launch_pdl(pack_stats_kernel, dim3(blocks), dim3(1024), 0, (cudaStream_t)stream, losses, done,
              episode_return, tb, status, seq_state, reinterpret_cast<uint8_t*>(out));
   return check_launch("pack_stats_kernel");
 }
