@@ -183,6 +183,11 @@ static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensor
     set_error("gemm: data-gradient epilogue needs a mask, bf16 out");
     return 1;
   }
+  if (EK == EPK_F32 && (!g.out_f32 || g.heads || g.bias || g.relu || g.mask_bits || g.bits_out || g.colsum ||
+                        g.alpha != 1.f)) {
+    set_error("gemm: EPK_F32 epilogue with unsupported features");
+    return BP_ERR_ARG;
+  }
   if (AW && (g.a_win_rows > 160 || g.a_win_rows < 128 || g.a_ntaps < 1 || g.a_ntaps > kMaxShifts)) {
     set_error("gemm: window rows %d / taps %d unsupported", g.a_win_rows, g.a_ntaps);
     return BP_ERR_ARG;
@@ -971,7 +976,7 @@ static int heads_backward(const BpAtariNet* net, int n, const float* d_logits, c
     g.colsum = ws + P.cs_off[3];
     return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_DGRAD>(g, ta, tb, s);
   }
-  return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
+  return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s);
 }
 
 // d_fc -> conv torso data / weight gradients, heads weight gradient (A operand head_in),
@@ -1034,7 +1039,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.cq = 1;
     g.cs1 = 3136;
     g.col_stride = 3136;
-    if ((rc = launch_gemm<128, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<128, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     // the fc weight gradient is final: the data-parallel learner may start its all-reduce
     if (net->fc_grad_ready && cudaEventRecord((cudaEvent_t)net->fc_grad_ready, s) != cudaSuccess) {
       set_error("atari backward: cudaEventRecord(fc_grad_ready) failed");
@@ -1111,10 +1116,10 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
     g.r_img = w.Npad;
     if (ncols == 32) {
       if ((r = make_tmap(&tb, dY, xrows, 32, 32, 64, 64))) return r;
-      return launch_gemm<32, A_MNMAJOR, B_MNMAJOR, 64>(g, ta, tb, s);
+      return launch_gemm<32, A_MNMAJOR, B_MNMAJOR, 64, false, 0, 0, EPK_F32>(g, ta, tb, s);
     }
     if ((r = make_tmap(&tb, dY, xrows, 64, 64, 64, 128))) return r;
-    return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s);
+    return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s);
   };
   // conv weight gradients, window kernel: X window + dY box per K-block feed every m-tile
   auto wgrad_win = [&](int i, const void* X, long long xrows, int xcols, int nshifts, const int* offs,
@@ -1441,7 +1446,7 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
     g.out_f32 = 1;
     g.out = core->gx;
     g.r_img = G4;
-    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128>(g, ta, tb, s))) return rc;
+    if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     const bool cl = lstm_use_cluster();
     const int pass = cl ? lstm_cluster_batch() : kLstmB;
     if (cl && (rc = lstm_cl_pack(params + off[l ? P_WHH1 : P_WHH0], H,
@@ -1588,7 +1593,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       g.out = core->wpart + (size_t)w * 2 * G4 * kCoreW;
       g.split_stride = (long long)G4 * kCoreW;
       g.r_img = kCoreW;
-      if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+      if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     }
     // input gradient: dx [n][576] = dgates [n][G4] . wih [G4][576]
     {
@@ -1604,7 +1609,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       g.out_f32 = 1;
       g.out = dx_out;
       g.r_img = kCoreW;
-      if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128>(g, ta, tb, s))) return rc;
+      if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     }
     lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)2 * G4 * kCoreW,
                                             (size_t)G4 * kCoreW,

@@ -258,7 +258,9 @@ BP_DEVICE float warp_transpose_sum(float (&v)[32], int lane) {
 //   EPK_HEADS the heads forward with the fused action sampler (inference only: the Philox code
 //             stays out of the EPK_GEN instantiations, where it cost the heads / fc gradient
 //             GEMMs 13 us per learner step in code size and registers).
-enum { EPK_GEN = 0, EPK_FWD = 1, EPK_DGRAD = 2, EPK_HEADS = 3 };
+//   EPK_F32   plain f32 output (split-K partials, weight gradients, LSTM projections), optional
+//             transposed store (col_stride); no bias / activation / mask / column sums.
+enum { EPK_GEN = 0, EPK_FWD = 1, EPK_DGRAD = 2, EPK_HEADS = 3, EPK_F32 = 4 };
 
 // element offset of column n (the column map; n is warp-uniform)
 BP_DEVICE long long col_offset(const GemmArgs& g, int n) {
@@ -278,6 +280,7 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
   if (n0 >= g.N) return;  // a partial last column tile (warp-uniform)
   const bool row_ok = roff >= 0;
   constexpr bool GEN = EK == EPK_GEN;
+  constexpr bool F32 = EK == EPK_F32;
   if ((GEN || EK == EPK_HEADS) && g.heads) {
     if (row_ok) {
 #pragma unroll
@@ -321,23 +324,23 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
   const long long coff = col_offset(g, n0);
   if (row_ok) {
     const long long off = roff + coff;
-    if (EK != EPK_DGRAD && g.bits_out) {
+    if (EK != EPK_DGRAD && !F32 && g.bits_out) {
       uint32_t bits = 0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) bits |= (v[i] > 0.f ? 1u : 0u) << i;
       g.bits_out[off >> 5] = bits;
     }
-    if (GEN && g.out_f32 && g.col_stride) {  // transposed store: per column, the warp's 32 rows are contiguous
+    if ((F32 || (GEN && g.out_f32)) && g.col_stride) {  // transposed store: per column, the warp's 32 rows are contiguous
       float* o = reinterpret_cast<float*>(g.out) + off;
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[(long long)i * g.col_stride] = v[i];
-    } else if (GEN && g.out_f32) {
+    } else if (F32 || (GEN && g.out_f32)) {
       float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(g.out) + off);
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
   }
-  if (!GEN || !g.out_f32) {
+  if (!F32 && (!GEN || !g.out_f32)) {
     // bf16 rows through a per-warp 2 KB staging buffer: every lane writes its 64-byte row chunk
     // (16-byte pieces XOR-swizzled by row pair: conflict-free), then each store instruction
     // writes 8 rows x 64 contiguous bytes (4 lanes per row) instead of 32 scattered 16-byte
@@ -362,7 +365,7 @@ BP_DEVICE void epilogue_chunk(const GemmArgs& g, long long roff, const long long
     }
     __syncwarp();  // the buffer is reused by the next chunk
   }
-  if (EK != EPK_FWD && g.colsum) {  // warp-uniform branch
+  if (EK != EPK_FWD && !F32 && g.colsum) {  // warp-uniform branch
     if (!row_ok) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
