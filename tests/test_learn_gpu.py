@@ -50,3 +50,33 @@ def test_learn_after_load_state_dict_uses_new_weights():
     total_ref, _, _ = atari_ref.learn_step(ref, ropt, {k: v.cpu() for k, v in batch.items()}, flags)
     stats = learner.learn(flags, None, net, batch, (), opt, None)  # graph replay path
     assert abs(stats["total_loss"] - total_ref) <= 1e-2 * max(1.0, abs(total_ref))
+
+
+def test_stats_after_several_unread_steps_and_in_place_batch_edit():
+    """stats() waits for the LATEST step's pack (completion word), also when several steps ran
+    without a stats read; an in-place edit of a batch tensor misses the memoised graph key
+    (version counter) and still replays the right graph (same addresses) with the new data."""
+    from paper_1910_03552_b200 import learner, optim
+    from paper_1910_03552_b200.atari_net import AtariNet
+
+    flags = dict(atari_ref.DEFAULT_FLAGS)
+    torch.manual_seed(4)
+    net = AtariNet(num_actions=6)
+    opt = optim.RMSprop(net.parameters(), lr=flags["learning_rate"], alpha=0.99, eps=0.01)
+    batch = {k: v.cuda() for k, v in atari_ref.synthetic_batch(8, 4, 6, seed=5).items()}
+    L = learner.FusedLearner(net, flags, 8, 4)
+    for _ in range(4):  # eager, capture + replay, replays; no stats read in between
+        L.step(batch, opt)
+    s1 = L.stats(batch)
+    torch.cuda.synchronize()
+    assert s1["total_loss"] == float(L.losses[3])
+    key = L._graph_key(batch, opt)
+    assert L._graph_key(batch, opt) is key  # memo hit
+    batch["reward"].mul_(0.5)  # in place: bumps the version counter, same address
+    key2 = L._graph_key(batch, opt)
+    assert key2 == key and key2 is not key
+    L.step(batch, opt)
+    s2 = L.stats(batch)
+    torch.cuda.synchronize()
+    assert s2["total_loss"] == float(L.losses[3])
+    assert len(L._graphs) == 1
