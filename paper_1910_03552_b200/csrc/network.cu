@@ -125,6 +125,16 @@ static GemmArgs base_args() {
 
 // conv weight gradients through the window kernel (umma_wgrad_win_kernel); 0 = per-tap
 // atom boxes through umma_gemm_kernel (BP_WGRAD_WINDOW=0 / bp_atari_set_wgrad_window)
+// small-batch inference tail (BP_SMALL_INFER=0: the GEMM fc epilogue + heads GEMM, A/B)
+static bool small_infer() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BP_SMALL_INFER");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static int g_wgrad_win = -1;
 static bool wgrad_window() {
   if (g_wgrad_win < 0) {
@@ -700,9 +710,11 @@ extern "C" int bp_atari_pack_weights(const BpAtariNet* net, const float* params,
 
 // frames -> conv torso -> fc -> augmented core [n][576] (net->core)
 // frames: u8 [n][4][84][84], or (plane_index != null) a plane store [num_planes][84][84]
+// fc_splitk > 1 (small-batch inference): the fc GEMM writes fc_splitk f32 split-K partials of
+// x3 . Wfc^T into the workspace instead of core[:, :512] (infer_heads_kernel finishes it)
 static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
                          int num_planes, const float* reward, const int64_t* last_action,
-                         const float* params, const int64_t* off, cudaStream_t s) {
+                         const float* params, const int64_t* off, cudaStream_t s, int fc_splitk = 1) {
   const int A = net->num_actions;
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
@@ -807,6 +819,25 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, true, 1, 0, EPK_FWD>(g, ta, tb, s))) return rc;
   }
   // 5. fc: X3 [n, 3136] x Wfc [512, 3136] -> core[:, :512] = relu(. + bfc)
+  if (fc_splitk > 1) {  // latency-bound small batches: K split over more CTAs, f32 partials
+    const int mt = (n + 127) / 128;
+    if ((rc = make_tmap(&ta, net->x3, n, 3136, 64, 128, 128))) return rc;
+    if ((rc = make_tmap(&tb, wbf + off[P_WFC], 512, 3136, 64, 64, 128))) return rc;
+    GemmArgs g = base_args();
+    g.m_tiles = mt;
+    g.n_tiles = 8;
+    g.splits = fc_splitk;
+    g.num_kb = 49;
+    g.kb_per_split = (49 + fc_splitk - 1) / fc_splitk;
+    g.a_cb = 49;
+    g.N = 512;
+    g.M = n;
+    g.out_f32 = 1;
+    g.out = net->ws;
+    g.split_stride = (long long)n * 512;
+    g.r_img = 512;
+    return launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s);
+  }
   {
     // 128-column tiles when 64-column ones would need a second wave: half the re-reads of
     // X3 from L2 (the fc GEMM is L2->SM bandwidth-bound) and a single wave
@@ -834,6 +865,52 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
 }
 
 // heads: head_in [n, 576] ([core | 1 | 0]) x Whf [32, 576] -> logits [n, A], baseline [n]
+// Small-batch inference tail (n <= kInferSmallN): one CTA per row finishes the split-K fc
+// (fixed-order sum of the partials + bias, ReLU, the bf16 rounding core[:, :512] has on the
+// GEMM path), appends the augmented columns prep wrote, and computes the A + 1 heads on CUDA
+// cores (bf16 operands, f32 accumulation: the same operands as the heads GEMM, a different
+// summation order) and the Gumbel-max action.  Replaces the fc epilogue + heads GEMM, whose
+// latency chains (3.2 MB of fc weights through 8 CTAs; 9 serial K-blocks in one CTA) dominate
+// small dynamic batches.
+constexpr int kInferSmallN = 256;  // (measured: k = 1 / 32 / 256 gain, k = 1024 does not)
+__global__ void __launch_bounds__(128) infer_heads_kernel(const float* __restrict__ part, int S, long long sstride,
+                                                          const float* __restrict__ bfc,
+                                                          const __nv_bfloat16* __restrict__ core,
+                                                          const __nv_bfloat16* __restrict__ whf, int A,
+                                                          float* __restrict__ logits, float* __restrict__ baseline,
+                                                          int64_t* __restrict__ actions, unsigned long long seed,
+                                                          const unsigned long long* __restrict__ seed_state,
+                                                          int greedy) {
+  pdl_wait();
+  __shared__ float c[kCoreW];
+  __shared__ float o[32];
+  const int r = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = tid; k < 512; k += 128) {
+    float acc = 0.f;
+    for (int q = 0; q < S; ++q) acc += part[(size_t)q * sstride + (size_t)r * 512 + k];
+    c[k] = __bfloat162float(__float2bfloat16_rn(fmaxf(acc + bfc[k], 0.f)));
+  }
+  for (int k = 512 + tid; k < kCoreW; k += 128) c[k] = __bfloat162float(core[(size_t)r * kCoreW + k]);
+  __syncthreads();
+  for (int a = warp; a <= A; a += 4) {
+    float acc = 0.f;
+    for (int k = lane; k < kCoreW; k += 32) acc = fmaf(c[k], __bfloat162float(whf[a * kCoreW + k]), acc);
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+    if (lane == 0) o[a] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = j <= A ? o[j] : 0.f;
+    for (int a = 0; a < A; ++a) logits[(size_t)r * A + a] = v[a];
+    baseline[r] = o[A];
+    if (actions)
+      actions[r] = gumbel_argmax<32>(v, A, seed_state ? *seed_state : seed, (unsigned long long)r, greedy != 0);
+  }
+}
+
 // fused action sampling of the heads epilogue (inference: bp_atari_forward_sample)
 struct SampleSpec {
   int64_t* actions;
@@ -905,6 +982,20 @@ static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   param_offsets(net->num_actions, 0, off);
   int rc;
   if ((rc = advance_seed(smp, s))) return rc;
+  // small inference batches (no backward follows): split-K fc + CUDA-core heads and sampling
+  const int mt = (n + 127) / 128;
+  int S = 148 / (mt * 8);
+  S = S > 7 ? 7 : S;
+  if (smp && (net->flags & BP_NET_NO_X0) && n <= kInferSmallN && S >= 2 && small_infer() &&
+      (size_t)S * n * 512 * sizeof(float) <= net->ws_bytes) {
+    if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s, S)))
+      return rc;
+    launch_pdl(infer_heads_kernel, dim3(n), dim3(128), 0, s, reinterpret_cast<const float*>(net->ws), S,
+               (long long)n * 512, params + off[P_BFC], reinterpret_cast<const __nv_bfloat16*>(net->core),
+               reinterpret_cast<const __nv_bfloat16*>(net->whf), net->num_actions, logits, baseline, smp->actions,
+               smp->seed, (const unsigned long long*)smp->seed_state, smp->greedy);
+    return check_launch("infer_heads_kernel");
+  }
   if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
     return rc;
   return heads_forward(net, n, net->core, logits, baseline, s, smp);
