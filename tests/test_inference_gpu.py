@@ -156,3 +156,28 @@ def test_lstm_actor_steps_equal_one_unroll_and_oracle():
     want = emu["policy_logits"]
     assert float((got - want).norm() / want.norm()) < 4e-3
     assert float((state[0].double().cpu() - st_emu[0]).norm() / st_emu[0].norm()) < 4e-3
+
+
+@pytest.mark.parametrize("k,A", [(1, 6), (100, 18), (256, 31)])
+def test_small_batch_inference_tail_matches_gemm_path(k, A):
+    """k <= 256: the split-K fc + CUDA-core heads tail (bp_atari_forward_sample) against the
+    tcgen05 fc epilogue + heads GEMM of the plain forward (same bf16 operands, different f32
+    summation order): logits / baseline within 1e-3 relative L2; against the bf16-emulating
+    oracle without adopting the kernel's near-zero ReLU decisions: 2e-3; greedy actions =
+    argmax of the returned logits."""
+    net, ref = _net(A, seed=8)
+    batch = atari_ref.synthetic_batch(0, k, A, seed=k + 3)
+    o = {key: v[0].cuda() for key, v in batch.items()}
+    actions = torch.empty(k, dtype=torch.int64, device="cuda")
+    small, sb = net._forward_kernels(o["frame"], o["reward"], o["last_action"], keep_x0=False,
+                                     actions=actions, seed=7, greedy=True, repack=True)
+    small, sb = small.clone(), sb.clone()
+    gemm, gb = net._forward_kernels(o["frame"], o["reward"], o["last_action"], keep_x0=True, repack=True)
+    rel = lambda a, b: float((a.double().cpu() - b.double().cpu()).norm() / b.double().cpu().norm())  # noqa: E731
+    assert rel(small, gemm) <= 1e-3 and rel(sb, gb) <= 1e-3
+    assert torch.equal(actions, small.argmax(1))
+    with torch.no_grad():
+        emu, _ = atari_ref.emulated_forward(ref.double(), {key: (v.double() if v.is_floating_point() else v)
+                                                           for key, v in batch.items()})
+    assert rel(small, emu["policy_logits"][0]) <= 2e-3
+    assert rel(sb, emu["baseline"][0]) <= 2e-3
