@@ -68,6 +68,7 @@ SIGNATURES: dict[str, tuple] = {
                                          P, P, P, P, P, P]),
     "bp_pack_stats": (I, [P, P, P, I, P, P, P, P]),
     "bp_host_wait_seq": (I, [P, C.c_uint, C.c_longlong]),
+    "bp_copy_many": (I, [P, P, P, I, P]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),
     "bp_infeed_get": (I, [P, P, P]),
     "bp_gemm_bf16_test": (I, [P, P, P, I, I, I, I, I, I, I, P]),

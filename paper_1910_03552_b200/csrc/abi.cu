@@ -64,3 +64,16 @@ extern "C" int bp_host_wait_seq(const unsigned* word, unsigned want, long long t
     }
   }
 }
+
+// Several device copies in one call (the inference graph path's input staging): dsts[i] <-
+// srcs[i], bytes[i], asynchronously on `stream` (device-to-device or pinned host).
+extern "C" int bp_copy_many(void* const* dsts, const void* const* srcs, const size_t* bytes, int n, void* stream) {
+  for (int i = 0; i < n; ++i) {
+    if (!bytes[i]) continue;
+    if (cudaMemcpyAsync(dsts[i], srcs[i], bytes[i], cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess) {
+      bp::set_error("bp_copy_many: copy %d failed: %s", i, cudaGetErrorString(cudaGetLastError()));
+      return BP_ERR_LAUNCH;
+    }
+  }
+  return BP_OK;
+}

@@ -21,7 +21,11 @@ an LSTM core the new core_state is returned as well (T = 1 actor step).
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import torch
+
+from . import _native as N
 
 from .errors import DimensionError
 
@@ -111,11 +115,14 @@ class ActorInference:
     # ------------------------------------------------------------------ graph path
     def _capture(self, b):
         m, dev, A = self.model, self.device, self.model.num_actions
+        # outputs packed in one buffer [actions b x i64 | logits b x A f32 | baseline b f32]: one
+        # clone per call returns them
+        outbuf = torch.empty(b * (8 + 4 * A + 4), dtype=torch.uint8, device=dev)
         st = dict(frames=torch.zeros(b, *m.observation_shape, dtype=torch.uint8, device=dev),
                   reward=torch.zeros(b, device=dev), last_action=torch.zeros(b, dtype=torch.int64, device=dev),
-                  done=torch.zeros(b, dtype=torch.uint8, device=dev),
-                  actions=torch.empty(b, dtype=torch.int64, device=dev), logits=torch.empty(b, A, device=dev),
-                  baseline=torch.empty(b, device=dev))
+                  done=torch.zeros(b, dtype=torch.uint8, device=dev), outbuf=outbuf,
+                  actions=outbuf[:8 * b].view(torch.int64), logits=outbuf[8 * b:8 * b + 4 * A * b].view(torch.float32).view(b, A),
+                  baseline=outbuf[8 * b + 4 * A * b:].view(torch.float32))
         if m.use_lstm:
             shape = (2, b, m.core_hidden)
             st.update(h0=torch.zeros(shape, device=dev), c0=torch.zeros(shape, device=dev),
@@ -145,15 +152,23 @@ class ActorInference:
         if ent is None or ent[2] != m.buffer_generation:
             ent = self._capture(b)
         graph, st, _ = ent
-        st["frames"][:k].copy_(frames)
-        st["reward"][:k].copy_(reward)
-        st["last_action"][:k].copy_(last_action)
+        # the inputs into the bucket's static buffers: one native call for every copy
+        pairs = [(st["frames"], frames), (st["reward"], reward), (st["last_action"], last_action)]
         if m.use_lstm:
-            st["done"][:k].copy_(done)
+            pairs.append((st["done"], done))
+        n = len(pairs)
+        dsts, srcs, nbytes = (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_size_t * n)()
+        for i, (d, src) in enumerate(pairs):
+            dsts[i], srcs[i], nbytes[i] = d.data_ptr(), src.data_ptr(), src.numel() * src.element_size()
+        N.check(N.lib().bp_copy_many(dsts, srcs, nbytes, n, torch.cuda.current_stream(self.device).cuda_stream),
+                "bp_copy_many")
+        if m.use_lstm:  # (strided (2, k, H) slices: torch copies)
             st["h0"][:, :k].copy_(h0)
             st["c0"][:, :k].copy_(c0)
         graph.replay()
         state = None
         if m.use_lstm:
             state = (st["hN"][:, :k].clone(), st["cN"][:, :k].clone())
-        return st["actions"][:k].clone(), st["logits"][:k].clone(), st["baseline"][:k].clone(), state
+        A, out = m.num_actions, st["outbuf"].clone()
+        return (out[:8 * b].view(torch.int64)[:k], out[8 * b:8 * b + 4 * A * b].view(torch.float32).view(b, A)[:k],
+                out[8 * b + 4 * A * b:].view(torch.float32)[:k], state)
