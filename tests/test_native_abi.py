@@ -57,3 +57,17 @@ def test_ops_fail_loudly_without_gpu(lib_path):
     z = torch.zeros(2, 1)
     with pytest.raises(NativeError):
         vtrace.from_importance_weights(z, z, z, z, torch.zeros(1))
+
+
+def test_host_wait_seq_without_gpu(lib_path):
+    """bp_host_wait_seq (the learner's stats wait) is host-only: reached / wrap-around / timeout."""
+    from paper_1910_03552_b200 import _native
+
+    lib = _native.load(lib_path)
+    word = ctypes.c_uint32(7)
+    addr = ctypes.addressof(word)
+    assert lib.bp_host_wait_seq(addr, 7, 1000) == 0      # reached
+    assert lib.bp_host_wait_seq(addr, 5, 1000) == 0      # already past
+    assert lib.bp_host_wait_seq(addr, 8, 2000) == 1      # not yet: times out
+    word.value = 2                                       # wrapped past 2^32
+    assert lib.bp_host_wait_seq(addr, 0xFFFFFFFE, 1000) == 0
