@@ -318,7 +318,7 @@ typedef struct BpLstmCore {
   float* dh;      /* [N][576] f32                                            */
   float* dx;      /* [N][576] f32                                            */
   float* wpart;   /* [2][2][G4][576] f32 weight-gradient GEMM outputs (W_ih, W_hh)
-                     x (split-K halves)                                       */
+                     x (split-K parts)                                        */
 } BpLstmCore;
 size_t bp_lstm_partial_floats(int hidden);
 /* Recurrence implementation: 0 auto (16-CTA cluster kernels with W_hh in registers and

@@ -82,7 +82,7 @@ class _LstmBuffers:
             dgates=torch.zeros(n, G4, dtype=bf, device=d),
             dh=torch.empty(n, 576, dtype=f32, device=d),
             dx=torch.empty(n, 576, dtype=f32, device=d),
-            wpart=torch.empty(2, 2, G4, 576, dtype=f32, device=d),
+            wpart=torch.empty(2, 2, G4, 576, dtype=f32, device=d),  # W_ih / W_hh x split-K parts
         )
         names = ("wih", "gx", "gates", "cseq", "hprev", "out", "hx", "part", "dgates", "dh", "dx", "wpart")
         self.struct = N.BpLstmCore(H, capacity, *[self.t[k].data_ptr() for k in names])

@@ -1415,6 +1415,11 @@ __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float*
 
 // weight-gradient GEMM outputs [G4][576] -> torch-layout grads of one layer
 // (two split-K halves, `half` elements apart, summed in a fixed order)
+#ifndef BP_LSTM_WG_SPLITS
+#define BP_LSTM_WG_SPLITS 2
+#endif
+constexpr int kLstmWgSplits = BP_LSTM_WG_SPLITS;  // split-K of the LSTM weight-gradient GEMMs (4: no faster)
+
 __global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* __restrict__ phh, size_t half,
                                     float* __restrict__ gwih, float* __restrict__ gwhh,
                                     float* __restrict__ gbih, float* __restrict__ gbhh, int H) {
@@ -1424,12 +1429,20 @@ __global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* 
   const int rp = (r % H) * 4 + r / H;
   for (int k = threadIdx.x; k < H; k += blockDim.x) {
     const size_t o = (size_t)rp * kCoreW + k;
-    gwih[(size_t)r * H + k] = pih[o] + pih[o + half];
-    gwhh[(size_t)r * H + k] = phh[o] + phh[o + half];
+    float si = pih[o], sh = phh[o];
+#pragma unroll
+    for (int q = 1; q < kLstmWgSplits; ++q) {  // fixed order
+      si += pih[o + q * half];
+      sh += phh[o + q * half];
+    }
+    gwih[(size_t)r * H + k] = si;
+    gwhh[(size_t)r * H + k] = sh;
   }
   if (threadIdx.x == 0) {
     const size_t o = (size_t)rp * kCoreW + H;
-    const float b = pih[o] + pih[o + half];
+    float b = pih[o];
+#pragma unroll
+    for (int q = 1; q < kLstmWgSplits; ++q) b += pih[o + q * half];
     gbih[r] = b;
     gbhh[r] = b;
   }
@@ -1671,17 +1684,17 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       GemmArgs g = base_args();
       g.m_tiles = G4 / 128;
       g.n_tiles = kCoreW / 64;
-      // split-K 2 (the lstm_scatter_kernel sums the halves): 17 x 9 = 153 tiles would need a
-      // second wave for 5 tiles on 148 SMs; 306 half-K tiles fill three half-length waves
-      g.splits = 2;
+      // split-K (the lstm_scatter_kernel sums the parts in a fixed order): 17 x 9 = 153 tiles
+      // would need a second wave for 5 tiles on 148 SMs
+      g.splits = kLstmWgSplits;
       g.num_kb = (n + 63) / 64;
-      g.kb_per_split = (g.num_kb + 1) / 2;
+      g.kb_per_split = (g.num_kb + kLstmWgSplits - 1) / kLstmWgSplits;
       g.a_atoms_per_shift = G4 / 64;
       g.a_nshifts = 1;
       g.N = kCoreW;
       g.M = G4;
       g.out_f32 = 1;
-      g.out = core->wpart + (size_t)w * 2 * G4 * kCoreW;
+      g.out = core->wpart + (size_t)w * kLstmWgSplits * G4 * kCoreW;
       g.split_stride = (long long)G4 * kCoreW;
       g.r_img = kCoreW;
       if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
@@ -1702,7 +1715,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       g.r_img = kCoreW;
       if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     }
-    lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)2 * G4 * kCoreW,
+    lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)kLstmWgSplits * G4 * kCoreW,
                                             (size_t)G4 * kCoreW,
                                             grads + off[l ? P_WIH1 : P_WIH0], grads + off[l ? P_WHH1 : P_WHH0],
                                             grads + off[l ? P_BIH1 : P_BIH0], grads + off[l ? P_BHH1 : P_BHH0], H);
