@@ -11,5 +11,5 @@ timeout 300 ncu --metrics $M --clock-control none -s 80 -c 90 --csv --log-file g
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo "ncu bench rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:lstm_cl_fwd -c 1 -o gpurun_out/r02/full_lstm_fwd python tools/prof_step.py 1 1 > /dev/null 2>&1; echo "f lstm rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:vt3_kernel -c 2 -o gpurun_out/r02/full_vt3_4096 python tools/vt_one.py 4096 > /dev/null 2>&1; echo "f vt3 rc=$?"
-for w in cfg1 cfg3 inf1 inf1024 cfg4s; do timeout 300 python tools/graph_kernels.py 5 $w > gpurun_out/r02/graph_kernels_$w.txt 2>&1; done; echo graphs done
+for w in cfg1 cfg3 inf1 inf1024 cfg4s; do timeout 300 python tools/graph_kernels.py 5 $w > gpurun_out/r02/graph_kernels_$w.txt 2>&1; done; timeout 300 python tools/graph_kernels.py 1 cfg4 > gpurun_out/r02/graph_kernels_cfg4.txt 2>&1; echo graphs done
 ls gpurun_out/r02
