@@ -389,8 +389,8 @@ int bp_infeed_get(void* stream, void* release_event, void* ready_event);
  * system-wide: the host can spin on it instead of synchronising on an event. */
 int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
                   unsigned* status, unsigned* seq_state, void* out, void* stream);
-/* n asynchronous copies dsts[i] <- srcs[i] (bytes[i] each, any direction) on stream, in one call
- * (ActorInference's graph path stages its inputs with it). */
+/* n <= 8 asynchronous copies dsts[i] <- srcs[i] (bytes[i] each; device or mapped pinned memory)
+ * on stream as one kernel launch (ActorInference's graph path stages its inputs with it). */
 int bp_copy_many(void* const* dsts, const void* const* srcs, const size_t* bytes, int n, void* stream);
 /* Host-side wait for a completion word in pinned host memory, e.g. the seq word of
  * bp_pack_stats: returns 0 once (*word - want) mod 2^32 < 2^31, 1 after timeout_us. */

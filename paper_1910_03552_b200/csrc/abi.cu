@@ -65,15 +65,51 @@ extern "C" int bp_host_wait_seq(const unsigned* word, unsigned want, long long t
   }
 }
 
-// Several device copies in one call (the inference graph path's input staging): dsts[i] <-
-// srcs[i], bytes[i], asynchronously on `stream` (device-to-device or pinned host).
-extern "C" int bp_copy_many(void* const* dsts, const void* const* srcs, const size_t* bytes, int n, void* stream) {
-  for (int i = 0; i < n; ++i) {
-    if (!bytes[i]) continue;
-    if (cudaMemcpyAsync(dsts[i], srcs[i], bytes[i], cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess) {
-      bp::set_error("bp_copy_many: copy %d failed: %s", i, cudaGetErrorString(cudaGetLastError()));
-      return BP_ERR_LAUNCH;
+// Several copies in one call (the inference graph path's input staging): dsts[i] <- srcs[i],
+// bytes[i], on `stream`, as ONE kernel launch (device or mapped pinned memory; 16-byte pieces
+// when both ends allow it), instead of one driver copy per buffer.
+namespace {
+constexpr int kMaxCopies = 8;
+struct CopyList {
+  void* dst[kMaxCopies];
+  const void* src[kMaxCopies];
+  size_t bytes[kMaxCopies];
+  int n;
+};
+__global__ void copy_many_kernel(const __grid_constant__ CopyList L) {
+  for (int c = 0; c < L.n; ++c) {
+    const size_t nb = L.bytes[c];
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(L.dst[c]) | reinterpret_cast<uintptr_t>(L.src[c]) | nb) & 15u) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(L.src[c]);
+      uint4* d4 = reinterpret_cast<uint4*>(L.dst[c]);
+      for (size_t i = i0; i < nb / 16; i += st) d4[i] = s4[i];
+    } else {
+      const uint8_t* s1 = reinterpret_cast<const uint8_t*>(L.src[c]);
+      uint8_t* d1 = reinterpret_cast<uint8_t*>(L.dst[c]);
+      for (size_t i = i0; i < nb; i += st) d1[i] = s1[i];
     }
   }
-  return BP_OK;
+}
+}  // namespace
+
+extern "C" int bp_copy_many(void* const* dsts, const void* const* srcs, const size_t* bytes, int n, void* stream) {
+  if (n < 0 || n > kMaxCopies) {
+    bp::set_error("bp_copy_many: 0 <= n <= %d", kMaxCopies);
+    return BP_ERR_ARG;
+  }
+  CopyList L;
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    L.dst[i] = dsts[i];
+    L.src[i] = srcs[i];
+    L.bytes[i] = bytes[i];
+    total += bytes[i];
+  }
+  L.n = n;
+  if (total == 0) return BP_OK;
+  size_t blocks = (total / 16 + 255) / 256;
+  blocks = blocks < 1 ? 1 : blocks > 296 ? 296 : blocks;
+  copy_many_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(L);
+  return bp::check_launch("copy_many_kernel");
 }

@@ -41,6 +41,7 @@ class ActorInference:
         # device-resident sampling key of the graph replays (advanced by every replay)
         self.seed_state = torch.tensor([seed & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
         self._graphs: dict[int, tuple] = {}
+        self._mv: dict[int, tuple] = {}  # k -> (version, model_version tensor (1, k))
         if self.buckets:
             model.buffers_for(self.buckets[-1])
 
@@ -108,8 +109,11 @@ class ActorInference:
             state = self._run(frames, reward, last_action, done, h0, c0, actions, logits, baseline)
         else:
             actions, logits, baseline, state = self._replay(bucket, k, frames, reward, last_action, done, h0, c0)
+        mv = self._mv.get(k)
+        if mv is None or mv[0] != self.version:  # (cached per k: one fill when the version moves)
+            mv = self._mv[k] = (self.version, torch.full((1, k), self.version, dtype=torch.int64, device=self.device))
         out = dict(action=actions.view(1, k), policy_logits=logits.view(1, k, -1), baseline=baseline.view(1, k),
-                   model_version=torch.full((1, k), self.version, dtype=torch.int64, device=self.device))
+                   model_version=mv[1])
         return (out, tuple(state) if state is not None else tuple())
 
     # ------------------------------------------------------------------ graph path
@@ -152,16 +156,20 @@ class ActorInference:
         if ent is None or ent[2] != m.buffer_generation:
             ent = self._capture(b)
         graph, st, _ = ent
-        # the inputs into the bucket's static buffers: one native call for every copy
-        pairs = [(st["frames"], frames), (st["reward"], reward), (st["last_action"], last_action)]
-        if m.use_lstm:
-            pairs.append((st["done"], done))
-        n = len(pairs)
-        dsts, srcs, nbytes = (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_size_t * n)()
-        for i, (d, src) in enumerate(pairs):
-            dsts[i], srcs[i], nbytes[i] = d.data_ptr(), src.data_ptr(), src.numel() * src.element_size()
-        N.check(N.lib().bp_copy_many(dsts, srcs, nbytes, n, torch.cuda.current_stream(self.device).cuda_stream),
-                "bp_copy_many")
+        # the inputs into the bucket's static buffers: one native call, one copy kernel (the
+        # ctypes argument arrays are kept per bucket; only sources and sizes change)
+        srcs_t = (frames, reward, last_action, done) if m.use_lstm else (frames, reward, last_action)
+        arrs = st.get("_copy_args")
+        if arrs is None:
+            n = len(srcs_t)
+            dst_t = (st["frames"], st["reward"], st["last_action"], st["done"])[:n]
+            arrs = st["_copy_args"] = ((C.c_void_p * n)(*[d.data_ptr() for d in dst_t]), (C.c_void_p * n)(),
+                                       (C.c_size_t * n)(), n, N.lib().bp_copy_many)
+        dsts, srcs, nbytes, n, fn = arrs
+        for i, src in enumerate(srcs_t):
+            srcs[i] = src.data_ptr()
+            nbytes[i] = src.numel() * src.element_size()
+        N.check(fn(dsts, srcs, nbytes, n, torch.cuda.current_stream(self.device).cuda_stream), "bp_copy_many")
         if m.use_lstm:  # (strided (2, k, H) slices: torch copies)
             st["h0"][:, :k].copy_(h0)
             st["c0"][:, :k].copy_(c0)
