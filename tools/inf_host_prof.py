@@ -83,3 +83,23 @@ torch.cuda.synchronize()
 for key, v in parts.items():
     v.sort()
     print(f"  {key:8s} median {v[len(v) // 2] * 1e6:6.1f} us")
+# eager path (no graph buckets): host time per call and the Python hot spots
+eager = ActorInference(m)
+for _ in range(10):
+    eager(obs)
+torch.cuda.synchronize()
+ts = []
+for _ in range(200):
+    t0 = time.perf_counter()
+    eager(obs)
+    ts.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+ts.sort()
+print(f"eager host time per call (no sync) median {ts[100] * 1e6:.1f} us")
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(300):
+    eager(obs)
+pr.disable()
+torch.cuda.synchronize()
+pstats.Stats(pr).sort_stats("tottime").print_stats(16)
