@@ -3,6 +3,7 @@ per-kernel mean device time over replays and the idle gaps between kernels.
 
     python tools/graph_kernels.py [REPLAYS]
 """
+import collections
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -48,12 +49,14 @@ for e in ev:
     cur.append(e)
 steps.append(cur)
 steps = [s for s in steps if s and "prep_kernel" in s[0].name]
-k = len(steps[0])
-print(f"{len(steps)} replays, {k} kernels per step")
+k = collections.Counter(len(s) for s in steps).most_common(1)[0][0]  # the usual kernel count
+full = [s for s in steps if len(s) == k]
+print(f"{len(steps)} replays ({len(full)} with the usual {k} kernels per step)")
+steps = full
 tot = 0.0
 for i in range(k):
-    d = sum(s[i].time_range.elapsed_us() for s in steps if len(s) == k) / len(steps)
-    gap = sum((s[i].time_range.start - s[i - 1].time_range.end) for s in steps if len(s) == k and i > 0) / len(steps)
+    d = sum(s[i].time_range.elapsed_us() for s in steps) / len(steps)
+    gap = sum((s[i].time_range.start - s[i - 1].time_range.end) for s in steps if i > 0) / len(steps)
     tot += d
     print(f"{i:3d} {d:8.1f} us  gap-before {gap:6.1f}  {steps[0][i].name[:90]}")
 span = sum(s[-1].time_range.end - s[0].time_range.start for s in steps) / len(steps)
