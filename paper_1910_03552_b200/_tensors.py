@@ -1,6 +1,9 @@
 """Small host helpers: numpy/torch in, contiguous CUDA tensors out."""
 from __future__ import annotations
 
+import contextlib
+import gc
+
 import numpy as np
 import torch
 
@@ -8,6 +11,24 @@ from ._native import require_cuda
 from .errors import SchemaError
 
 _status_words: dict[int, "object"] = {}
+
+
+@contextlib.contextmanager
+def graph_capture(graph, **kw):
+    """`torch.cuda.graph(graph, **kw)` with Python's cyclic garbage collector paused.
+
+    torch no longer collects garbage when a capture begins. An automatic collection that runs
+    mid-capture can finalise an unreachable CUDAGraph from earlier work, and destroying its
+    executable is an unsafe call that invalidates a global-mode capture. Seen as "operation
+    failed due to a previous error during capture" at the next launch."""
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        with torch.cuda.graph(graph, **kw):
+            yield
+    finally:
+        if enabled:
+            gc.enable()
 
 
 def status_word(device: torch.device):

@@ -28,6 +28,7 @@ import torch
 from . import _native as N
 
 from .errors import DimensionError
+from ._tensors import graph_capture
 
 
 class ActorInference:
@@ -144,7 +145,7 @@ class ActorInference:
             body()  # warm-up: lazy init (tensor maps, function attributes) outside the capture
         torch.cuda.current_stream(dev).wait_stream(s)
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        with graph_capture(graph):
             body()
         self.seed_state.copy_(saved)
         self._graphs[b] = (graph, st, m.buffer_generation)

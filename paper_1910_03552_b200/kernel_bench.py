@@ -20,6 +20,8 @@ import os
 
 import torch
 
+from paper_1910_03552_b200._tensors import graph_capture
+
 
 def _peaks():
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -49,7 +51,7 @@ class Timer:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 fn()
-                with torch.cuda.graph(g, stream=side):
+                with graph_capture(g, stream=side):
                     fn()
             torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
@@ -83,7 +85,7 @@ class Timer:
         side.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
+            with graph_capture(g, stream=side):
                 for _ in range(reps):
                     for f in fns:
                         f()

@@ -28,6 +28,7 @@ import torch
 from . import _native as N  # noqa: F401  (fail loudly if the library is missing)
 from .errors import NONFINITE_GRAD, NONFINITE_IN, NONFINITE_LOSS, SchemaError, StatusWord, raise_for_bits
 from .learner_ops import LearnerLoss, VtraceConfig
+from ._tensors import graph_capture
 from .optim import RMSprop, sumsq_
 
 # learner-input fields and their dtypes (upstream learn() batch; validate_batch rollout.py:160-192)
@@ -231,7 +232,7 @@ class FusedLearner:
                 side.wait_stream(torch.cuda.current_stream())
                 c0 = N.lib().bp_launch_count()
                 try:
-                    with torch.cuda.graph(g, stream=side):
+                    with graph_capture(g, stream=side):
                         self._step_eager(batch, optimizer)
                 except (RuntimeError, torch.cuda.CudaError) as exc:
                     if self.pg is None:

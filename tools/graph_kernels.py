@@ -4,6 +4,7 @@ per-kernel mean device time over replays and the idle gaps between kernels.
     python tools/graph_kernels.py [REPLAYS]
 """
 import collections
+import os
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -36,11 +37,20 @@ else:
 for _ in range(4):
     run()
 torch.cuda.synchronize()
+bg = int(os.environ.get("BP_GK_H2D_MB", "0"))  # background pinned H2D copies (e2e contention)
+if bg:
+    hbuf = torch.empty(bg << 20, dtype=torch.uint8, pin_memory=True)
+    dbuf = torch.empty(bg << 20, dtype=torch.uint8, device=dev)
+    cstream = torch.cuda.Stream()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    if bg:
+        with torch.cuda.stream(cstream):
+            for _ in range(reps * 2):
+                dbuf.copy_(hbuf, non_blocking=True)
     for _ in range(reps):
         run()
     torch.cuda.synchronize()
-ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA" and not e.name.startswith("Memcpy")], key=lambda e: e.time_range.start)
 steps, cur = [], []
 for e in ev:
     if "prep_kernel" in e.name and cur:
