@@ -382,13 +382,16 @@ int bp_infeed_get(void* stream, void* release_event, void* ready_event);
  * finished episodes): packs losses [4] f64, done [tb] u8 and episode_return [tb] f32
  * (nullable) and the status word (nullable; read, then cleared for the next step) into
  * out = [32 B losses | 4 B status | 4 B seq | tb B done | tb * 4 B returns] in one launch.
+ * sumsq (nullable): the step's squared gradient norm; a non-finite value with a finite total
+ * loss (losses[3]) adds BP_STATUS_NONFINITE_GRAD, the verdict bp_rmsprop_clip_f32 reaches from
+ * the same inputs -- so the pack can run concurrently with an update given status = NULL.
  * out may be device memory or pinned host memory (written through its unified-address
  * mapping: the step's result reaches the host without a separate copy).  seq_state
  * (nullable; 2 x u32 device memory, zeroed once) makes the pack publish a completion
  * sequence number in the seq word (1, 2, ... per call) after all its other writes are visible
  * system-wide: the host can spin on it instead of synchronising on an event. */
 int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                  unsigned* status, unsigned* seq_state, void* out, void* stream);
+                  unsigned* status, const double* sumsq, unsigned* seq_state, void* out, void* stream);
 /* n <= 8 asynchronous copies dsts[i] <- srcs[i] (bytes[i] each; device or mapped pinned memory)
  * on stream as one kernel launch (ActorInference's graph path stages its inputs with it). */
 int bp_copy_many(void* const* dsts, const void* const* srcs, const size_t* bytes, int n, void* stream);

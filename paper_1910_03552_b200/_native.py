@@ -66,7 +66,7 @@ SIGNATURES: dict[str, tuple] = {
     "bp_atari_forward_sample": (I, [P, I, P, P, I, P, P, P, C.c_uint64, P, I, P, P, P, P]),
     "bp_atari_lstm_forward_sample": (I, [P, P, I, I, P, P, I, P, P, P, P, P, P, C.c_uint64, P, I,
                                          P, P, P, P, P, P]),
-    "bp_pack_stats": (I, [P, P, P, I, P, P, P, P]),
+    "bp_pack_stats": (I, [P, P, P, I, P, P, P, P, P]),
     "bp_host_wait_seq": (I, [P, C.c_uint, C.c_longlong]),
     "bp_copy_many": (I, [P, P, P, I, P]),
     "bp_infeed_put": (I, [P, P, C.c_size_t, P, P, P]),

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(1024) pack_stats_kernel(const double* __restri
                                                          const uint8_t* __restrict__ done,
                                                          const float* __restrict__ ret, int tb,
                                                          unsigned* __restrict__ status,
+                                                         const double* __restrict__ sumsq,
                                                          unsigned* __restrict__ seq_state,
                                                          uint8_t* __restrict__ out) {
   pdl_wait();
@@ -171,6 +172,9 @@ __global__ void __launch_bounds__(1024) pack_stats_kernel(const double* __restri
       st = *status;
       *status = 0u;
     }
+    // the optimiser's verdict, derived from the same inputs it uses (rmsprop_kernel: a
+    // non-finite norm with a finite total loss), so this pack may run beside the update
+    if (sumsq && !isfinite(*sumsq) && isfinite(losses[3])) st |= BP_STATUS_NONFINITE_GRAD;
     reinterpret_cast<unsigned*>(out)[8] = st;
   }
   for (int i = i0; i < tb; i += gridDim.x * blockDim.x) {  // (few blocks: one system fence each)
@@ -217,7 +221,8 @@ __global__ void __launch_bounds__(1024) pack_stats_kernel(const double* __restri
 using namespace bp;
 
 extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const float* episode_return, int tb,
-                             unsigned* status, unsigned* seq_state, void* out, void* stream) {
+                             unsigned* status, const double* sumsq, unsigned* seq_state, void* out,
+                             void* stream) {
   if (!losses || !done || !out || tb < 0) {
     set_error("pack_stats: bad args");
     return BP_ERR_ARG;
@@ -225,7 +230,7 @@ extern "C" int bp_pack_stats(const double* losses, const uint8_t* done, const fl
   const int n = tb > 5 ? tb : 5;
   const int blocks = (n + 8191) / 8192;  // 1024 threads x <= 8 elements per block
   launch_pdl(pack_stats_kernel, dim3(blocks), dim3(1024), 0, (cudaStream_t)stream, losses, done,
-             episode_return, tb, status, seq_state, reinterpret_cast<uint8_t*>(out));
+             episode_return, tb, status, sumsq, seq_state, reinterpret_cast<uint8_t*>(out));
   return check_launch("pack_stats_kernel");
 }
 

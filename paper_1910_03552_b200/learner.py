@@ -86,6 +86,7 @@ class FusedLearner:
         self._np_seq = hnp[36:40].view(np.uint32)
         self._np_seq[0] = 0
         self._seq_state = torch.zeros(2, dtype=torch.int32, device=dev)
+        self._pack_stream = torch.cuda.Stream(device=dev)  # the stats pack beside the update
         self._packs = 0  # packs enqueued (graph replays included)
         self._seq_addr = self._stats_host.data_ptr() + 36
         self._c_wait = N.lib().bp_host_wait_seq
@@ -333,10 +334,26 @@ class FusedLearner:
         #    the device (model.py:251-252: parameters untouched); stats() then raises
         if optimizer is not None:
             if isinstance(optimizer, RMSprop) and optimizer.flat_params.data_ptr() == m.flat_params.data_ptr():
+                # the stats pack forks off once the gradient norm is reduced and runs beside the
+                # update: it derives the update's reject verdict from the same norm + loss, so
+                # the host's read-back (and its turnaround to the next step) overlaps the
+                # RMSProp pass instead of trailing it.  (Measured alternatives: the pack beside
+                # the backward delays a persistent GEMM's CTA; copy-engine copies of the stats
+                # as graph memcpy nodes cost ~10 us per step.)
+                cur = torch.cuda.current_stream()
+                side = self._pack_stream
+
+                def fork_pack(sumsq):
+                    side.wait_stream(cur)
+                    with torch.cuda.stream(side):
+                        self._pack_stats(batch, self.losses, sumsq=sumsq)
+
                 optimizer.step(max_norm=self.max_norm, mirror=m.flat_bf16,  # params + bf16 mirror
-                               status=self.status, reject_if_nonfinite=self.losses[3:])
+                               status=False, reject_if_nonfinite=self.losses[3:], on_norm=fork_pack)
+                cur.wait_stream(side)
                 m.mirror_fresh = True
                 m._packed_version = m.flat_params._version
+                return self.losses
             else:  # any torch optimiser: check the step first (one sync), then clip + its own step
                 bits = self.status.bits()
                 if bits or not bool(torch.isfinite(self.losses[3])):
@@ -351,7 +368,7 @@ class FusedLearner:
         self._pack_stats(batch, self.losses)
         return self.losses
 
-    def _pack_stats(self, batch, losses):
+    def _pack_stats(self, batch, losses, sumsq=None):
         """Loss vector, done[1:] and episode_return[1:] -> the pinned read-back buffer, written
         by one kernel through the device mapping of the pinned host memory (unified virtual
         addressing).  Part of the step (and of its CUDA graph)."""
@@ -369,7 +386,8 @@ class FusedLearner:
         if not torch.cuda.is_current_stream_capturing():  # (a capture runs nothing; replays count)
             self._packs += 1
         N.check(N.lib().bp_pack_stats(losses.data_ptr(), done.data_ptr(), ep.data_ptr() if ep is not None else None,
-                                      tb, self.status.ptr(), self._seq_state.data_ptr(), host.data_ptr(),
+                                      tb, self.status.ptr(), sumsq.data_ptr() if sumsq is not None else None,
+                                      self._seq_state.data_ptr(), host.data_ptr(),
                                       N.stream_handle(losses.device)),
                 "bp_pack_stats")
 

@@ -54,12 +54,14 @@ def rmsprop_clip_(params: torch.Tensor, grads: torch.Tensor, square_avg: torch.T
                   reject_if_nonfinite: torch.Tensor | None = None) -> None:
     """In-place clip + RMSProp over flat buffers, norm read from `sumsq` on device.
     reject_if_nonfinite: a device f64 scalar (the step's total loss); non-finite -> the
-    whole update is rejected on device, like a non-finite gradient norm."""
-    sw = status if status is not None else status_word(params.device)
+    whole update is rejected on device, like a non-finite gradient norm.
+    status: the StatusWord for BP_STATUS_NONFINITE_GRAD (None: the per-device word; False: none,
+    e.g. when a concurrent stats pack derives the bit from `sumsq` itself)."""
+    sw = None if status is False else status if status is not None else status_word(params.device)
     N.check(N.lib().bp_rmsprop_clip_f32(
         N.ptr(params), N.ptr(grads), N.ptr(square_avg), params.numel(), N.ptr(sumsq),
         float(max_norm), CLIP_MODES[clip_mode], float(lr), N.ptr(lr_dev), float(alpha),
-        float(eps), int(write_clipped_grads), N.ptr(norm_out), N.ptr(mirror), sw.ptr(),
+        float(eps), int(write_clipped_grads), N.ptr(norm_out), N.ptr(mirror), sw.ptr() if sw else None,
         N.ptr(reject_if_nonfinite), N.stream_handle(params.device)), "bp_rmsprop_clip_f32")
 
 
@@ -157,10 +159,12 @@ class RMSprop(torch.optim.Optimizer):
 
     @torch.no_grad()
     def step(self, closure=None, max_norm: float | None = None, mirror: torch.Tensor | None = None,
-             status=None, reject_if_nonfinite: torch.Tensor | None = None):
+             status=None, reject_if_nonfinite: torch.Tensor | None = None, on_norm=None):
         """One fused clip + RMSProp update.  status: the StatusWord that receives
-        BP_STATUS_NONFINITE_GRAD (default: the per-device word); reject_if_nonfinite: a device
-        f64 scalar (the learner step's total loss) whose non-finite value rejects the update."""
+        BP_STATUS_NONFINITE_GRAD (default: the per-device word; False: none); reject_if_nonfinite:
+        a device f64 scalar (the learner step's total loss) whose non-finite value rejects the
+        update; on_norm(sumsq): called once the squared-norm reduction is enqueued, before the
+        update (the learner forks its stats pack there)."""
         loss = closure() if closure is not None else None
         if not torch.cuda.is_current_stream_capturing():
             self.sync_lr()
@@ -170,6 +174,8 @@ class RMSprop(torch.optim.Optimizer):
         elif not self._sumsq_zero:
             self._sumsq.zero_()
         self._sumsq_zero = mode == "none"
+        if on_norm is not None:
+            on_norm(self._sumsq)
         g = self.param_groups[0]
         rmsprop_clip_(self.flat_params, self.flat_grads, self.square_avg, self._sumsq,
                       lr=g["lr"], alpha=g["alpha"], eps=g["eps"],

@@ -134,3 +134,26 @@ def test_buffer_reallocation_drops_captured_graphs():
     stats = learner.learn(flags, None, net, batch, (), opt, None)
     assert len(L._graphs) == 0 and np.isfinite(stats["total_loss"])
     assert not torch.equal(net.flat_params, p_before)
+
+
+@pytest.mark.parametrize("sumsq,total,want", [(float("inf"), 1.0, 16), (float("nan"), 1.0, 16),
+                                              (4.0, 1.0, 0), (float("inf"), float("nan"), 0)])
+def test_stats_pack_derives_the_update_verdict(sumsq, total, want):
+    """The pack beside the RMSProp update reports BP_STATUS_NONFINITE_GRAD exactly when the
+    update rejects for a non-finite norm (rmsprop_kernel: non-finite norm, finite total loss;
+    a non-finite total is reported by the loss kernel's own bit instead)."""
+    from paper_1910_03552_b200 import _native as N
+
+    tb = 8
+    losses = torch.tensor([0.5, 0.25, -0.1, total], dtype=torch.float64, device="cuda")
+    done = torch.zeros(tb, dtype=torch.uint8, device="cuda")
+    ss = torch.tensor([sumsq], dtype=torch.float64, device="cuda")
+    status = torch.tensor([4], dtype=torch.int32, device="cuda")  # a bit the loss kernel set
+    seq = torch.zeros(2, dtype=torch.int32, device="cuda")
+    out = torch.zeros(40 + 5 * tb, dtype=torch.uint8).pin_memory()
+    N.check(N.lib().bp_pack_stats(losses.data_ptr(), done.data_ptr(), None, tb, status.data_ptr(), ss.data_ptr(),
+                                  seq.data_ptr(), out.data_ptr(), N.stream_handle()), "bp_pack_stats")
+    torch.cuda.synchronize()
+    words = out[:40].numpy().view(np.uint32)
+    assert words[8] == 4 | want and words[9] == 1
+    assert int(status.item()) == 0  # read, then cleared for the next step
