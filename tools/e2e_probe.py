@@ -69,9 +69,17 @@ L = learner.FusedLearner(model, bench.FLAGS, T, B)
 for _ in range(3):
     L.step(src[0], opt)
 torch.cuda.synchronize()
-for label in ("alone", "under copies"):
+import ctypes  # noqa: E402
+rt = ctypes.CDLL("libcuda.so.1")
+for label in ("alone", "under copies", "alone (uploaded)", "under copies (uploaded)"):
+    if "uploaded" in label and rt is not None:
+        for g in L._graphs.values():
+            rc = rt.cuGraphUpload(ctypes.c_void_p(g.raw_cuda_graph_exec()),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            print("cuGraphUpload rc", rc)
+        torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if label != "alone":
+    if "under" in label:
         e0, e1 = copies(N)
     s0.record()
     for _ in range(30):
