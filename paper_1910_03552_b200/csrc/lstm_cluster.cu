@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_fwd_kernel(const __grid_co
   const uint32_t ld_base = smem_u32(&S.hT[0][lane][0]);
   const int ncols = a.B - cb < NB ? a.B - cb : NB;
   cluster_sync_all();  // every CTA running, barriers initialised, before any DSMEM traffic
+  // every CTA resident: a PDL-launched successor that does not read this kernel's output (the
+  // next layer's weight packing, lstm_cl_pack / pack_lstm_wih) may start on the free SMs now
+  pdl_trigger();
   if (trace) trace[4 * a.T1 * 2 + 1] = gtimer();
   // the step records {i, f, g, o, c} leave through one 4D TMA store per step (issued by thread
   // STORE_TID, asynchronous: no global-store instructions on the recurrent critical path); the
@@ -493,7 +496,10 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
 // frag[dir][rank][warp][item][kstep][reg][lane] (u32 = 2 bf16), dir 0 forward (rows = own
 // gate rows, K = hidden), dir 1 backward (rows = hidden, K = own gate rows).  Run once per
 // weight update; the kernels then load their ~108 fragment registers with coalesced loads.
+// PDL: reads only the parameters, so it starts early (beside the previous layer's recurrence)
+// and waits for its predecessor only at the end -- completion stays transitive for the chain
 __global__ void lstm_cl_pack_kernel(const float* __restrict__ whh, int H, uint32_t* __restrict__ frag) {
+  pdl_trigger();
   constexpr int PER_WARP = ITEMS * KSMAX * 4 * 32;
   constexpr int PER_DIR = CS * WARPS * PER_WARP;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * PER_DIR; i += gridDim.x * blockDim.x) {
@@ -525,6 +531,7 @@ __global__ void lstm_cl_pack_kernel(const float* __restrict__ whh, int H, uint32
     }
     frag[i] = pack2(v0, v1);
   }
+  pdl_wait();
 }
 
 size_t lstm_cl_frag_words() { return (size_t)2 * CS * WARPS * ITEMS * KSMAX * 4 * 32; }
@@ -532,7 +539,8 @@ size_t lstm_cl_frag_dir_words() { return (size_t)CS * WARPS * ITEMS * KSMAX * 4 
 
 int lstm_cl_pack(const float* whh, int H, uint32_t* frag, cudaStream_t s) {
   // one word per thread: the per-word index math and scattered W_hh reads are latency-bound
-  lstm_cl_pack_kernel<<<(unsigned)((lstm_cl_frag_words() + 255) / 256), 256, 0, s>>>(whh, H, frag);
+  launch_pdl(lstm_cl_pack_kernel, dim3((unsigned)((lstm_cl_frag_words() + 255) / 256)), dim3(256), 0, s, whh, H,
+             frag);
   return check_launch("lstm_cl_pack_kernel");
 }
 

@@ -1403,6 +1403,8 @@ __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float*
   // one block per output row, one bf16 pair per thread (coalesced row reads / writes).
   // Output row rp = j * 4 + gate holds torch row r = gate * H + j: the gate-interleaved G4
   // order of gx, dgates and the weight-gradient rows (an owner's 4 gates are contiguous)
+  // PDL: parameters only -- starts early, waits for its predecessor at the end (as lstm_cl_pack)
+  pdl_trigger();
   const int rp = blockIdx.x, k = 2 * threadIdx.x;
   const int r = rp < 4 * H ? (rp & 3) * H + (rp >> 2) : 4 * H;
   auto val = [&](int kk) {
@@ -1411,6 +1413,7 @@ __global__ void pack_lstm_wih_kernel(const float* __restrict__ wih, const float*
   };
   reinterpret_cast<__nv_bfloat162*>(dst + (size_t)rp * kCoreW)[threadIdx.x] =
       __floats2bfloat162_rn(val(k), val(k + 1));
+  pdl_wait();
 }
 
 // weight-gradient GEMM outputs [G4][576] -> torch-layout grads of one layer
@@ -1525,16 +1528,26 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
     return rc;
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(core->wih);
   const size_t wsz = (size_t)G4 * kCoreW;
-  for (int l = 0; l < 2; ++l) {
+  // layer l's input-weight operand; layer 1's packing (and its W_hh fragments below) run as
+  // PDL successors of layer 0's recurrence, on the SMs its clusters leave free
+  auto pack_wih = [&](int l) {
     const int pw = l ? P_WIH1 : P_WIH0, pb = l ? P_BIH1 : P_BIH0, pc = l ? P_BHH1 : P_BHH0;
-    pack_lstm_wih_kernel<<<G4, kCoreW / 2, 0, s>>>(params + off[pw], params + off[pb], params + off[pc], wih + l * wsz,
-                                             H, G4);
-    if ((rc = check_launch("pack_lstm_wih_kernel"))) return rc;
-  }
+    launch_pdl(pack_lstm_wih_kernel, dim3(G4), dim3(kCoreW / 2), 0, s, params + off[pw], params + off[pb],
+               params + off[pc], wih + l * wsz, H, G4);
+    return check_launch("pack_lstm_wih_kernel");
+  };
+  if ((rc = pack_wih(0))) return rc;
   auto bfp = [&](void* base, int l) {
     return reinterpret_cast<__nv_bfloat16*>(base) + (size_t)l * core->max_rows * kCoreW;
   };
+  const bool cl = lstm_use_cluster();
   for (int l = 0; l < 2; ++l) {
+    if (l == 1) {
+      if (cl && (rc = lstm_cl_pack(params + off[P_WHH1], H,
+                                   reinterpret_cast<uint32_t*>(core->part) + lstm_cl_frag_words(), s)))
+        return rc;
+      if ((rc = pack_wih(1))) return rc;
+    }
     // gx [n][G4] = x_aug [n][576] . wih^T (biases through the ones column)
     CUtensorMap ta, tb;
     const void* x = l ? (const void*)bfp(core->out, 0) : net->core;
@@ -1551,10 +1564,8 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
     g.out = core->gx;
     g.r_img = G4;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
-    const bool cl = lstm_use_cluster();
     const int pass = cl ? lstm_cluster_batch() : kLstmB;
-    if (cl && (rc = lstm_cl_pack(params + off[l ? P_WHH1 : P_WHH0], H,
-                                 reinterpret_cast<uint32_t*>(core->part) + (size_t)l * lstm_cl_frag_words(), s)))
+    if (l == 0 && cl && (rc = lstm_cl_pack(params + off[P_WHH0], H, reinterpret_cast<uint32_t*>(core->part), s)))
       return rc;
     for (int b0 = 0; b0 < B; b0 += pass) {
       LstmFwdArgs a;
