@@ -314,7 +314,7 @@ typedef struct BpLstmCore {
   float* part;    /* bp_lstm_partial_floats(H): cooperative-path exchange, or the
                      cluster path's packed W_hh fragments (written by the forward,
                      read by the backward of the same step)                */
-  void* dgates;   /* [N][G4] bf16 pre-activation gate gradients, zeroed once */
+  void* dgates;   /* [2][N][G4] bf16 pre-activation gate gradients per layer, zeroed once */
   float* dh;      /* [N][576] f32                                            */
   float* dx;      /* [N][576] f32                                            */
   float* wpart;   /* [2][2][G4][576] f32 weight-gradient GEMM outputs (W_ih, W_hh)

@@ -79,7 +79,7 @@ class _LstmBuffers:
             out=torch.zeros(2, n, 576, dtype=bf, device=d),
             hx=torch.empty(2, H, 32, dtype=f32, device=d),
             part=torch.empty(N.lib().bp_lstm_partial_floats(H), dtype=f32, device=d),
-            dgates=torch.zeros(n, G4, dtype=bf, device=d),
+            dgates=torch.zeros(2, n, G4, dtype=bf, device=d),  # per layer
             dh=torch.empty(n, 576, dtype=f32, device=d),
             dx=torch.empty(n, 576, dtype=f32, device=d),
             wpart=torch.empty(2, 2, G4, 576, dtype=f32, device=d),  # W_ih / W_hh x split-K parts

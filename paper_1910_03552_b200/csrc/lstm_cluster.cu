@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1) lstm_cl_bwd_kernel(const LstmBwdAr
   // ldmatrix row address: matrix m = lane / 8 -> (k-step +m/2, k half m%2), row n = lane % 8
   const uint32_t ld_base = smem_u32(&S.dz[lane & 7][((lane >> 3) & 1) * 8 + (lane >> 4) * 16]);
   cluster_sync_all();
+  pdl_trigger();  // every CTA resident: the previous layer's weight gradients may start beside
 
   // the owner's inputs of step tt, prefetched one step ahead (issued after the previous
   // step's owner math, so no global load sits in front of the recurrent MMAs)

@@ -216,7 +216,8 @@ static int launch_gemm(const GemmArgs& g0, const CUtensorMap& ta, const CUtensor
     attr = true;
   }
   const int tiles = g.m_tiles * g.n_tiles * g.splits;
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int cap = g.max_ctas > 0 && g.max_ctas < g_num_sms ? g.max_ctas : g_num_sms;
+  const int grid = tiles < cap ? tiles : cap;
   launch_pdl(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, g, ta, tb);
   return check_launch("umma_gemm_kernel");
 }
@@ -1659,11 +1660,13 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   const size_t wsz = (size_t)G4 * kCoreW;
   // d(out[1]) [n][576] f32 from the heads
   if ((rc = heads_backward(net, n, d_logits, d_baseline, P, ws, core->dh, s))) return rc;
-  for (int l = 1; l >= 0; --l) {
-    float* dh_in = l == 1 ? core->dh : core->dx;   // gradient w.r.t. this layer's output
-    float* dx_out = l == 1 ? core->dx : core->dh;  // gradient w.r.t. this layer's input
-    const bool cl = lstm_use_cluster();
-    const int pass = cl ? lstm_cluster_batch() : kLstmB;
+  const bool cl = lstm_use_cluster();
+  const int pass = cl ? lstm_cluster_batch() : kLstmB;
+  auto dgates = [&](int l) {  // per layer: layer 1's weight gradients read it beside layer 0's recurrence
+    return reinterpret_cast<__nv_bfloat16*>(core->dgates) + (size_t)l * core->max_rows * G4;
+  };
+  // the recurrence of layer l (gradient w.r.t. its output: dh_in) -> dgates(l)
+  auto recur = [&](int l, const float* dh_in) -> int {
     for (int b0 = 0; b0 < B; b0 += pass) {
       LstmBwdArgs a;
       a.H = H;
@@ -1680,18 +1683,23 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       a.dh_out = dh_in;
       a.dh_ld = kCoreW;
       a.part = core->part;
-      a.dgates = reinterpret_cast<__nv_bfloat16*>(core->dgates);
+      a.dgates = dgates(l);
       a.dg_ld = G4;
       a.wfrag = reinterpret_cast<const uint32_t*>(core->part) + (size_t)l * lstm_cl_frag_words() +
                 lstm_cl_frag_dir_words();
-      if ((rc = cl ? lstm_cl_launch_bwd(a, s) : lstm_launch_bwd(a, s))) return rc;
+      if (int r = cl ? lstm_cl_launch_bwd(a, s) : lstm_launch_bwd(a, s)) return r;
     }
+    return BP_OK;
+  };
+  // weight gradients of layer l: D[r][k] = sum_rows dgates[row][r] * X[row][k], X = layer input /
+  // previous state.  beside > 0: PDL successors of layer 0's recurrence on at most `beside` CTAs
+  // each (the SMs its clusters leave free), waiting for it only at their end
+  auto wgrads = [&](int l, int beside) -> int {
     CUtensorMap ta, tb;
-    // weight gradients: D[r][k] = sum_rows dgates[row][r] * X[row][k], X = layer input / previous state
     for (int w = 0; w < 2; ++w) {
       const void* X = w == 0 ? (l ? (const void*)bfp(core->out, 0) : net->core) : (const void*)bfp(core->hprev, l);
-      if ((rc = make_tmap(&ta, core->dgates, n, G4, 64, 64, 128))) return rc;
-      if ((rc = make_tmap(&tb, X, n, kCoreW, 64, 64, 128))) return rc;
+      if (int r = make_tmap(&ta, dgates(l), n, G4, 64, 64, 128)) return r;
+      if (int r = make_tmap(&tb, X, n, kCoreW, 64, 64, 128)) return r;
       GemmArgs g = base_args();
       g.m_tiles = G4 / 128;
       g.n_tiles = kCoreW / 64;
@@ -1708,30 +1716,45 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       g.out = core->wpart + (size_t)w * kLstmWgSplits * G4 * kCoreW;
       g.split_stride = (long long)G4 * kCoreW;
       g.r_img = kCoreW;
-      if ((rc = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
-    }
-    // input gradient: dx [n][576] = dgates [n][G4] . wih [G4][576]
-    {
-      if ((rc = make_tmap(&ta, core->dgates, n, G4, 64, 128, 128))) return rc;
-      if ((rc = make_tmap(&tb, wih + l * wsz, G4, kCoreW, 64, 64, 128))) return rc;
-      GemmArgs g = base_args();
-      g.m_tiles = (n + 127) / 128;
-      g.n_tiles = kCoreW / 64;
-      g.num_kb = g.kb_per_split = G4 / 64;
-      g.a_cb = G4 / 64;
-      g.N = kCoreW;
-      g.M = n;
-      g.out_f32 = 1;
-      g.out = dx_out;
-      g.r_img = kCoreW;
-      if ((rc = launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
+      if (beside > 0) {
+        g.max_ctas = beside;
+        g.pdl_late = 1;
+      }
+      if (int r = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s)) return r;
     }
     lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)kLstmWgSplits * G4 * kCoreW,
                                             (size_t)G4 * kCoreW,
                                             grads + off[l ? P_WIH1 : P_WIH0], grads + off[l ? P_WHH1 : P_WHH0],
                                             grads + off[l ? P_BIH1 : P_BIH0], grads + off[l ? P_BHH1 : P_BHH0], H);
-    if ((rc = check_launch("lstm_scatter_kernel"))) return rc;
-  }
+    return check_launch("lstm_scatter_kernel");
+  };
+  // input gradient of layer l: dx [n][576] = dgates [n][G4] . wih [G4][576]
+  auto dgrad = [&](int l, float* dx_out) -> int {
+    CUtensorMap ta, tb;
+    if (int r = make_tmap(&ta, dgates(l), n, G4, 64, 128, 128)) return r;
+    if (int r = make_tmap(&tb, wih + l * wsz, G4, kCoreW, 64, 64, 128)) return r;
+    GemmArgs g = base_args();
+    g.m_tiles = (n + 127) / 128;
+    g.n_tiles = kCoreW / 64;
+    g.num_kb = g.kb_per_split = G4 / 64;
+    g.a_cb = G4 / 64;
+    g.N = kCoreW;
+    g.M = n;
+    g.out_f32 = 1;
+    g.out = dx_out;
+    g.r_img = kCoreW;
+    return launch_gemm<64, A_KMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s);
+  };
+  // layer 1, then layer 0's recurrence with layer 1's weight gradients beside it (cluster path:
+  // the recurrence occupies ceil(B / 8) x 16 SMs); dh: d(out[1]) from the heads, dx: d(out[0])
+  const int busy = cl ? ((pass < B ? pass : B) + 7) / 8 * 16 : g_num_sms;
+  const int spare = (g_num_sms - busy) / 2;  // per weight-gradient GEMM (two run side by side)
+  if ((rc = recur(1, core->dh))) return rc;
+  if ((rc = dgrad(1, core->dx))) return rc;
+  if ((rc = recur(0, core->dx))) return rc;
+  if ((rc = wgrads(1, cl && B <= pass && spare >= 8 ? spare : 0))) return rc;
+  if ((rc = dgrad(0, core->dh))) return rc;
+  if ((rc = wgrads(0, 0))) return rc;
   // layer-0 input gradient (core->dh) -> d_fc (relu mask) + bias partials for dbfc
   lstm_dfc_kernel<<<dim3(P.cs_rows[3], 4), 128, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
                                                reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);

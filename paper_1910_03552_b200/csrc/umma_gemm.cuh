@@ -40,6 +40,10 @@ inline FDiv fdiv_make(uint32_t d) {
 BP_DEVICE uint32_t fdivu(uint32_t n, FDiv f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 
 struct GemmArgs {
+  // launch: grid cap (0 = one CTA per SM); pdl_late: the inputs are final before this kernel's
+  // PDL predecessor started (e.g. the LSTM layer-1 weight gradients beside layer 0's
+  // recurrence), so the kernel runs at once and waits for its predecessor only at the end
+  int max_ctas, pdl_late;
   // tiling
   int m_tiles, n_tiles, splits;
   int num_kb;        // K blocks in total (K / 64 for K-major, rows / 64 for MN-major)
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // the previous kernel's outputs (every global read below)
+  if (!g.pdl_late) pdl_wait();  // the previous kernel's outputs (every global read below)
 
   const int ntiles = g.m_tiles * g.n_tiles * g.splits;
   // Warps 0 (TMA producer) and 1 (MMA issuer) run their loops converged with
@@ -910,6 +914,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  if (g.pdl_late) pdl_wait();  // completion stays transitive for the kernels after this one
 }
 
 // ============================================================================
