@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
                                                    __nv_bfloat16* __restrict__ whf, const float* __restrict__ reward,
                                                    const int64_t* __restrict__ last_action,
                                                    __nv_bfloat16* __restrict__ core, int n, int A) {
+  pdl_trigger();  // conv1 may launch now: it sets up its pipeline, then waits for this kernel
   pdl_wait();
   if (blockIdx.x < 36) {
     const int core_w = 513 + A;
