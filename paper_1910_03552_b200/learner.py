@@ -87,6 +87,7 @@ class FusedLearner:
         self._np_seq[0] = 0
         self._seq_state = torch.zeros(2, dtype=torch.int32, device=dev)
         self._pack_stream = torch.cuda.Stream(device=dev)  # the stats pack beside the update
+        self._state_zero = False  # LSTM: h0 / c0 staged buffers hold zeros
         self._packs = 0  # packs enqueued (graph replays included)
         self._seq_addr = self._stats_host.data_ptr() + 36
         self._c_wait = N.lib().bp_host_wait_seq
@@ -206,9 +207,11 @@ class FusedLearner:
             if len(initial_agent_state) == 2:
                 self.lstm["h0"].copy_(initial_agent_state[0])
                 self.lstm["c0"].copy_(initial_agent_state[1])
-            else:
+                self._state_zero = False
+            elif not self._state_zero:  # (the step only reads h0 / c0: zero stays zero)
                 self.lstm["h0"].zero_()
                 self.lstm["c0"].zero_()
+                self._state_zero = True
         if self._buf_gen != self.model.buffer_generation:
             # the model reallocated its activation buffers (e.g. a larger forward): every
             # captured graph points at freed memory
