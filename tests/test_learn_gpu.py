@@ -80,3 +80,48 @@ def test_stats_after_several_unread_steps_and_in_place_batch_edit():
     torch.cuda.synchronize()
     assert s2["total_loss"] == float(L.losses[3])
     assert len(L._graphs) == 1
+
+
+def test_graph_capture_pauses_the_cyclic_collector():
+    """A CUDA graph that only a reference cycle keeps alive is destroyed whenever the cyclic
+    garbage collector runs; destroying a graph executable during a global-mode stream capture
+    invalidates that capture.  The learner's and the actor-inference captures therefore run in
+    _tensors.graph_capture, which pauses the automatic collector.  Here a graph becomes cyclic
+    garbage in the middle of a capture while the collector would run at every allocation."""
+    import gc
+
+    from paper_1910_03552_b200._tensors import graph_capture
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    x = torch.zeros(4, device="cuda")
+    dead = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(dead):
+            x.add_(1.0)
+    keep = [dead]
+    del dead
+
+    class Cycle:
+        pass
+
+    g = torch.cuda.CUDAGraph()
+    thresholds = gc.get_threshold()
+    gc.set_threshold(1, 1, 1)
+    try:
+        with torch.cuda.stream(s):
+            with graph_capture(g):
+                x.mul_(2.0)
+                c = Cycle()
+                c.graph, c.self = keep.pop(), c
+                del c
+                junk = [[i] for i in range(2000)]  # the automatic collector would run here
+                del junk
+                x.add_(3.0)
+    finally:
+        gc.set_threshold(*thresholds)
+    torch.cuda.current_stream().wait_stream(s)
+    x.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x.cpu(), torch.full((4,), 3.0))
