@@ -1081,9 +1081,41 @@ struct FrameSrc {
   int num_planes;
 };
 
+// heads weight gradient: split-K partials of head_in^T . G (the finalize reduces them).
+// beside > 0: a PDL successor of the LSTM's layer-1 backward recurrence on at most `beside`
+// CTAs, waiting for it only at its end (its inputs are final before that recurrence starts)
+static int heads_wgrad(const BpAtariNet* net, int n, const void* head_in, const NetPlan& P, float* ws,
+                       cudaStream_t s, int beside) {
+  const WgPlan& w = P.wg[3];
+  CUtensorMap ta, tb;
+  int r;
+  if ((r = make_tmap(&ta, head_in, n, kCoreW, 64, 64, 128))) return r;
+  if ((r = make_tmap(&tb, net->g, n, 64, 64, 64, 128))) return r;
+  GemmArgs g = base_args();
+  g.m_tiles = w.m_tiles;
+  g.n_tiles = w.n_tiles;
+  g.splits = w.splits;
+  g.num_kb = w.num_kb;
+  g.kb_per_split = w.kb_per;
+  g.a_atoms_per_shift = kCoreW / 64;
+  g.a_nshifts = 1;
+  g.a_row_off[0] = 0;
+  g.N = w.Npad;
+  g.M = (int)w.Mpad;
+  g.out_f32 = 1;
+  g.out = ws + w.off;
+  g.split_stride = w.Mpad * w.Npad;
+  g.r_img = w.Npad;
+  if (beside > 0) {
+    g.max_ctas = beside;
+    g.pdl_late = 1;
+  }
+  return launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s);
+}
+
 static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, const void* head_in, float* grads,
                           const int64_t* off,
-                          const NetPlan& P, float* ws, cudaStream_t s) {
+                          const NetPlan& P, float* ws, cudaStream_t s, bool heads_wgrad_done = false) {
   const int A = net->num_actions;
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   int rc;
@@ -1296,8 +1328,7 @@ static int torso_backward(const BpAtariNet* net, int n, const FrameSrc* src, con
       if ((rc = wgrad(1, net->x1, (long long)n * 100, 128, 2, 4, o2, net->d_pre2, 64))) return rc;
       if ((rc = wgrad(2, net->x2, (long long)n * 81, 64, 1, 9, o3, net->d_pre3, 64))) return rc;
     }
-    const int o0[1] = {0};
-    if ((rc = wgrad(3, head_in, n, kCoreW, kCoreW / 64, 1, o0, net->g, 64))) return rc;
+    if (!heads_wgrad_done && (rc = heads_wgrad(net, n, head_in, P, ws, s, 0))) return rc;
   }
   // deterministic finalize: conv weight grads (transpose to [Cout][K]), heads, biases
   {
@@ -1751,6 +1782,9 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   const int busy = cl ? ((pass < B ? pass : B) + 7) / 8 * 16 : g_num_sms;
   const int spare = (g_num_sms - busy) / 2;  // per weight-gradient GEMM (two run side by side)
   if ((rc = recur(1, core->dh))) return rc;
+  // the heads weight gradient needs only G and layer 1's output: beside layer 1's recurrence
+  const bool beside = cl && B <= pass && g_num_sms - busy >= 16;
+  if (beside && (rc = heads_wgrad(net, n, bfp(core->out, 1), P, ws, s, g_num_sms - busy))) return rc;
   if ((rc = dgrad(1, core->dx))) return rc;
   if ((rc = recur(0, core->dx))) return rc;
   if ((rc = wgrads(1, cl && B <= pass && spare >= 8 ? spare : 0))) return rc;
@@ -1760,7 +1794,7 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   lstm_dfc_kernel<<<dim3(P.cs_rows[3], 4), 128, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
                                                reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);
   if ((rc = check_launch("lstm_dfc_kernel"))) return rc;
-  return torso_backward(net, n, nullptr, bfp(core->out, 1), grads, off, P, ws, s);
+  return torso_backward(net, n, nullptr, bfp(core->out, 1), grads, off, P, ws, s, beside);
 }
 
 // ============================================================ action sampling
