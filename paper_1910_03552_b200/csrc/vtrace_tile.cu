@@ -476,9 +476,11 @@ int vt3_launch(bool loss, const float* beh, const float* tgt, const int64_t* act
     return e ? std::atoi(e) : 0;
   }();
   // columns per tile: BT * A * 4 bytes per TMA box row must be a multiple of 16
-  // from_logits at large B streams best with 8-column tiles (fewer, longer TMA rows)
+  // from_logits at large B streams best with 8-column tiles (fewer, longer TMA rows; T=80 A=18
+  // B=4096: 13.2 vs 13.8 us with 4-column tiles, B=16384: 40.6 vs 43.9 us); the loss mode is
+  // the same at 4 or 8 columns (24.2 / 24.8 us at B=4096, tools/vt3_sweep.py)
   // small B (the per-GPU learner batch) is latency-bound: 2-column tiles double the CTAs
-  int kBT = bt_env ? bt_env : (!loss && B >= 16384 && B % 8 == 0) ? 8 : (B <= 256 && B % 2 == 0) ? 2 : 4;
+  int kBT = bt_env ? bt_env : (!loss && B >= 4096 && B % 8 == 0) ? 8 : (B <= 256 && B % 2 == 0) ? 2 : 4;
   if (!(kBT == 2 || kBT == 4 || kBT == 8) || T * kBT > 992) kBT = 4;
   if (!(A == 6 || A == 18) || B % kBT || T > kMaxT || T * kBT > 992) return BP_ERR_UNSUPPORTED;
   const uintptr_t al = reinterpret_cast<uintptr_t>(beh) | reinterpret_cast<uintptr_t>(tgt) |
