@@ -722,12 +722,23 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
   int rc;
   // 1. frames -> space-to-depth bf16 (+ augmented core columns), heads operand
-  if (conv1_u8()) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
+  // prep folded into conv1 (default): the heads pack and the core columns run in conv1's idle
+  // warp 3 instead of a kernel of their own at the head of the chain (cfg1 step span 359.1 ->
+  // 356.8 us, cfg3 1245.2 -> 1241.6 us; env BP_PREP_FOLD=0: the separate prep_kernel)
+  static const bool prep_fold = [] {
+    const char* e = std::getenv("BP_PREP_FOLD");
+    return !(e && e[0] == '0');
+  }();
+  // (only when conv1 runs one CTA per SM: at small n its few CTAs would serialise the work --
+  // k=1 inference: conv1 5.2 -> 21.3 us folded)
+  if (int e = tma_init()) return e;  // (the SM count)
+  const bool fold = conv1_u8() && prep_fold && (long long)n * 441 >= 128LL * g_num_sms;
+  if (conv1_u8() && !fold) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
     launch_pdl(prep_kernel, dim3(36 + (n * 8 + 511) / 512), dim3(512), 0, s, params + off[P_WP],
                params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf), reward, last_action,
                bf(net->core), n, A);
     if ((rc = check_launch("prep_kernel"))) return rc;
-  } else {
+  } else if (!fold) {
     frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
                                              bf(net->core), A);
     if ((rc = check_launch("frames_s2d_kernel"))) return rc;
@@ -767,6 +778,9 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.bits_out = reinterpret_cast<uint32_t*>(net->m1);
     g.gh = 21; g.gw = 21; g.vh = 20; g.vw = 20; g.sy = 2; g.sx = 2;
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
+    if (fold)
+      g.prep = PrepArgs{params + off[P_WP], params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf),
+                        reward, last_action, bf(net->core), n, A};
     if (conv1_u8_mode() == 2) {
       if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 2, EPK_FWD>(g, ta, tb, s))) return rc;
     } else if (conv1_u8()) {

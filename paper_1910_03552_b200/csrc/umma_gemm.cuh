@@ -39,6 +39,52 @@ inline FDiv fdiv_make(uint32_t d) {
 }
 BP_DEVICE uint32_t fdivu(uint32_t n, FDiv f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 
+// the forward's two small jobs (network.cu prep_kernel): pack the heads operand
+// Whf [32][576] bf16 = [Wp | bp ; Wv | bv] and write the augmented core columns [512, 576)
+// [clip(r) | onehot(a) | 1 | 0] of every row.  Item space: [0, 32 * 576) heads elements, then
+// n * 8 core chunks of 8 columns (one 16-byte store each).
+struct PrepArgs {
+  const float *wp, *bp, *wv, *bv;
+  __nv_bfloat16* whf;
+  const float* reward;
+  const int64_t* last_action;
+  __nv_bfloat16* core;
+  int n, A;  // n == 0: no prep work
+};
+
+BP_DEVICE void prep_items(const PrepArgs& p, long long i0, long long stride) {
+  constexpr int W = 576;
+  const int core_w = 513 + p.A;
+  const long long nh = 32 * W, total = nh + (long long)p.n * 8;
+  for (long long i = i0; i < total; i += stride) {
+    if (i < nh) {
+      const int a = (int)(i / W), j = (int)(i % W);
+      float v = 0.f;
+      if (a < p.A) v = j < core_w ? p.wp[(size_t)a * core_w + j] : (j == core_w ? p.bp[a] : 0.f);
+      else if (a == p.A) v = j < core_w ? p.wv[j] : (j == core_w ? p.bv[0] : 0.f);
+      p.whf[i] = __float2bfloat16_rn(v);
+      continue;
+    }
+    const long long c = i - nh, img = c >> 3;
+    const int j0 = (int)(c & 7) * 8;
+    const float r = fminf(fmaxf(p.reward[img], -1.f), 1.f);
+    const long long la = p.last_action[img];
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = j0 + 2 * q + h;
+        v2[h] = j == 0 ? r : j <= p.A ? (la == j - 1 ? 1.f : 0.f) : (j == p.A + 1 ? 1.f : 0.f);
+      }
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(v2[0], v2[1]);
+      w[q] = *reinterpret_cast<const uint32_t*>(&b2);
+    }
+    *reinterpret_cast<uint4*>(p.core + img * W + 512 + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 struct GemmArgs {
   // launch: grid cap (0 = one CTA per SM); pdl_late: the inputs are final before this kernel's
   // PDL predecessor started (e.g. the LSTM layer-1 weight gradients beside layer 0's
@@ -106,6 +152,8 @@ struct GemmArgs {
   // epilogue divisors (filled by the launcher from gh*gw, gw, sy, sx, cdiv, cq)
   FDiv fd_per, fd_gw, fd_sy, fd_sx, fd_cdiv, fd_cq, fd_splits, fd_ntiles;
   long long col_stride;  // f32 output only: element stride between consecutive columns (0 = 1, vector stores)
+  PrepArgs prep;         // prep.n > 0: the idle warp 3 of every CTA also does the forward's prep
+                         // work (conv1: its outputs are read only by later kernels)
 };
 
 inline void gemm_prepare(GemmArgs& g) {
@@ -786,6 +834,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       if (++rs == kRawStages) { rs = 0; rph ^= 1; }
       if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
     }
+  } else if (warp == 3 && g.prep.n > 0) {
+    prep_items(g.prep, (long long)blockIdx.x * 32 + lane, (long long)gridDim.x * 32);
   } else if (warp >= 4 && warp < 4 + 4 * C::EPI) {
     // epilogue warpgroup grp takes the CTA's tiles k = grp, grp + EPI, ... (accumulator k % ACC);
     // warp ew of a group reads TMEM lanes [32 ew, 32 ew + 32)

@@ -51,14 +51,16 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
         run()
     torch.cuda.synchronize()
 ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA" and not e.name.startswith("Memcpy")], key=lambda e: e.time_range.start)
+# a step starts at prep_kernel, or (prep folded into conv1, the default) at the u8 conv1 GEMM
+first = "prep_kernel" if any("prep_kernel" in e.name for e in ev) else "umma_gemm_kernel<32, 0, 0, 128, true, 1, "
 steps, cur = [], []
 for e in ev:
-    if "prep_kernel" in e.name and cur:
+    if first in e.name and cur:
         steps.append(cur)
         cur = []
     cur.append(e)
 steps.append(cur)
-steps = [s for s in steps if s and "prep_kernel" in s[0].name]
+steps = [s for s in steps if s and first in s[0].name]
 k = collections.Counter(len(s) for s in steps).most_common(1)[0][0]  # the usual kernel count
 full = [s for s in steps if len(s) == k]
 print(f"{len(steps)} replays ({len(full)} with the usual {k} kernels per step)")
