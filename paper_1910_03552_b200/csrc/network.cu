@@ -1588,6 +1588,9 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
     return reinterpret_cast<__nv_bfloat16*>(base) + (size_t)l * core->max_rows * kCoreW;
   };
   const bool cl = lstm_use_cluster();
+  // layer 0's W_hh fragments: packed beside layer 0's W_ih operand (both read parameters only
+  // and start at their predecessor's trigger) instead of between the gx GEMM and the recurrence
+  if (cl && (rc = lstm_cl_pack(params + off[P_WHH0], H, reinterpret_cast<uint32_t*>(core->part), s))) return rc;
   for (int l = 0; l < 2; ++l) {
     if (l == 1) {
       if (cl && (rc = lstm_cl_pack(params + off[P_WHH1], H,
@@ -1612,8 +1615,6 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
     g.r_img = G4;
     if ((rc = launch_gemm<64, A_KMAJOR, B_KMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s))) return rc;
     const int pass = cl ? lstm_cluster_batch() : kLstmB;
-    if (l == 0 && cl && (rc = lstm_cl_pack(params + off[P_WHH0], H, reinterpret_cast<uint32_t*>(core->part), s)))
-      return rc;
     for (int b0 = 0; b0 < B; b0 += pass) {
       LstmFwdArgs a;
       a.H = H;
