@@ -937,6 +937,8 @@ struct SampleSpec {
 
 // graph-replayable sampling: every call advances the device-resident seed (splitmix64 step)
 __global__ void advance_seed_kernel(unsigned long long* seed_state) {
+  pdl_trigger();  // the forward's first kernel may launch now (it waits for this one)
+  pdl_wait();     // the previous call's sampler has read the seed
   unsigned long long x = *seed_state + 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
   x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
@@ -945,7 +947,7 @@ __global__ void advance_seed_kernel(unsigned long long* seed_state) {
 
 static int advance_seed(const SampleSpec* smp, cudaStream_t s) {
   if (!smp || !smp->seed_state) return BP_OK;
-  advance_seed_kernel<<<1, 1, 0, s>>>(smp->seed_state);
+  launch_pdl(advance_seed_kernel, dim3(1), dim3(1), 0, s, smp->seed_state);
   return check_launch("advance_seed_kernel");
 }
 
@@ -1475,6 +1477,8 @@ __global__ void lstm_scatter_kernel(const float* __restrict__ pih, const float* 
                                     float* __restrict__ gbih, float* __restrict__ gbhh, int H) {
   // one block per torch gate row r (= GEMM row rp = j * 4 + gate, gate-interleaved order),
   // threads over the hidden columns (coalesced)
+  pdl_trigger();  // the next GEMM may set up (it waits for this kernel)
+  pdl_wait();     // the weight-gradient partials
   const int r = blockIdx.x;
   const int rp = (r % H) * 4 + r / H;
   for (int k = threadIdx.x; k < H; k += blockDim.x) {
@@ -1504,6 +1508,8 @@ __global__ void __launch_bounds__(128) lstm_dfc_kernel(const float* __restrict__
                                                        __nv_bfloat16* __restrict__ d_fc,
                                                        float* __restrict__ colsum, int n) {
   // rows [32*grp, 32*grp + 32), one column per thread; the 32 loads are independent
+  pdl_trigger();  // the torso backward's first GEMM may set up (it waits for this kernel)
+  pdl_wait();     // the layer-0 input gradient
   const int grp = blockIdx.x, c = blockIdx.y * blockDim.x + threadIdx.x;
   float s = 0.f;
   const int rows = n - grp * 32 < 32 ? n - grp * 32 : 32;
@@ -1769,8 +1775,8 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
       }
       if (int r = launch_gemm<64, A_MNMAJOR, B_MNMAJOR, 128, false, 0, 0, EPK_F32>(g, ta, tb, s)) return r;
     }
-    lstm_scatter_kernel<<<4 * H, 288, 0, s>>>(core->wpart, core->wpart + (size_t)kLstmWgSplits * G4 * kCoreW,
-                                            (size_t)G4 * kCoreW,
+    launch_pdl(lstm_scatter_kernel, dim3(4 * H), dim3(288), 0, s, (const float*)core->wpart,
+               (const float*)(core->wpart + (size_t)kLstmWgSplits * G4 * kCoreW), (size_t)G4 * kCoreW,
                                             grads + off[l ? P_WIH1 : P_WIH0], grads + off[l ? P_WHH1 : P_WHH0],
                                             grads + off[l ? P_BIH1 : P_BIH0], grads + off[l ? P_BHH1 : P_BHH0], H);
     return check_launch("lstm_scatter_kernel");
@@ -1806,8 +1812,9 @@ extern "C" int bp_atari_lstm_backward(const BpAtariNet* net, const BpLstmCore* c
   if ((rc = dgrad(0, core->dh))) return rc;
   if ((rc = wgrads(0, 0))) return rc;
   // layer-0 input gradient (core->dh) -> d_fc (relu mask) + bias partials for dbfc
-  lstm_dfc_kernel<<<dim3(P.cs_rows[3], 4), 128, 0, s>>>(core->dh, reinterpret_cast<const uint32_t*>(net->mc),
-                                               reinterpret_cast<__nv_bfloat16*>(net->d_fc), ws + P.cs_off[3], n);
+  launch_pdl(lstm_dfc_kernel, dim3(P.cs_rows[3], 4), dim3(128), 0, s, (const float*)core->dh,
+             reinterpret_cast<const uint32_t*>(net->mc), reinterpret_cast<__nv_bfloat16*>(net->d_fc),
+             ws + P.cs_off[3], n);
   if ((rc = check_launch("lstm_dfc_kernel"))) return rc;
   return torso_backward(net, n, nullptr, bfp(core->out, 1), grads, off, P, ws, s, beside);
 }
