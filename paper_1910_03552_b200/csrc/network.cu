@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
 // G [N][64] bf16 = [d_logits (A) | d_baseline | 0 ...]
 __global__ void pack_g_kernel(const float* __restrict__ dlog, const float* __restrict__ dbase,
                               __nv_bfloat16* __restrict__ G, int n, int A) {
+  pdl_trigger();  // the heads data-gradient GEMM may set up (it waits for this kernel)
   pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 8-col chunk)
   if (i >= (long long)n * 8) return;

@@ -193,6 +193,9 @@ template <int A, int kBT, bool LOSS>
 __global__ void __launch_bounds__(1024) vt3_kernel(const __grid_constant__ Args g,
                                                    const __grid_constant__ Maps mp) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  // persistent grid (every CTA resident at once): the next kernel (the learner's G pack) may
+  // launch now; it waits for this kernel before reading its outputs
+  pdl_trigger();
   pdl_wait();
   constexpr int RS = kBT * A;  // floats per tile row
   const int T = g.T, B = g.B, nch = g.nchunks;
