@@ -283,9 +283,11 @@ __global__ void __launch_bounds__(512) prep_kernel(const float* __restrict__ wp,
                                                    const float* __restrict__ wv, const float* __restrict__ bv,
                                                    __nv_bfloat16* __restrict__ whf, const float* __restrict__ reward,
                                                    const int64_t* __restrict__ last_action,
-                                                   __nv_bfloat16* __restrict__ core, int n, int A) {
+                                                   __nv_bfloat16* __restrict__ core, int n, int A,
+                                                   unsigned long long* seed_state) {
   pdl_trigger();  // conv1 may launch now: it sets up its pipeline, then waits for this kernel
   pdl_wait();
+  if (seed_state && blockIdx.x == 0 && threadIdx.x == 0) advance_seed_dev(seed_state);  // (sampling)
   if (blockIdx.x < 36) {
     const int core_w = 513 + A;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * kCoreW; i += 36 * blockDim.x) {
@@ -715,9 +717,12 @@ extern "C" int bp_atari_pack_weights(const BpAtariNet* net, const float* params,
 // frames: u8 [n][4][84][84], or (plane_index != null) a plane store [num_planes][84][84]
 // fc_splitk > 1 (small-batch inference): the fc GEMM writes fc_splitk f32 split-K partials of
 // x3 . Wfc^T into the workspace instead of core[:, :512] (infer_heads_kernel finishes it)
+__global__ void advance_seed_kernel(unsigned long long* seed_state);
+
 static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, const int32_t* plane_index,
                          int num_planes, const float* reward, const int64_t* last_action,
-                         const float* params, const int64_t* off, cudaStream_t s, int fc_splitk = 1) {
+                         const float* params, const int64_t* off, cudaStream_t s, int fc_splitk = 1,
+                         unsigned long long* seed_state = nullptr) {
   const int A = net->num_actions;
   const __nv_bfloat16* wbf = reinterpret_cast<const __nv_bfloat16*>(net->wbf);
   auto bf = [](void* p) { return reinterpret_cast<__nv_bfloat16*>(p); };
@@ -737,9 +742,13 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   if (conv1_u8() && !fold) {  // conv1 converts the frames on chip (and writes X0 for the weight gradient)
     launch_pdl(prep_kernel, dim3(36 + (n * 8 + 511) / 512), dim3(512), 0, s, params + off[P_WP],
                params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf), reward, last_action,
-               bf(net->core), n, A);
+               bf(net->core), n, A, seed_state);
     if ((rc = check_launch("prep_kernel"))) return rc;
   } else if (!fold) {
+    if (seed_state) {
+      launch_pdl(advance_seed_kernel, dim3(1), dim3(1), 0, s, seed_state);
+      if ((rc = check_launch("advance_seed_kernel"))) return rc;
+    }
     frames_s2d_kernel<<<n * 21, 128, 0, s>>>(frames, plane_index, num_planes, bf(net->x0), reward, last_action,
                                              bf(net->core), A);
     if ((rc = check_launch("frames_s2d_kernel"))) return rc;
@@ -781,7 +790,7 @@ static int torso_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
     g.r_img = 100 * 128; g.r_y = 10 * 128; g.r_x = 128; g.r_sub = 32;
     if (fold)
       g.prep = PrepArgs{params + off[P_WP], params + off[P_BP], params + off[P_WV], params + off[P_BV], bf(net->whf),
-                        reward, last_action, bf(net->core), n, A};
+                        reward, last_action, bf(net->core), n, A, seed_state};
     if (conv1_u8_mode() == 2) {
       if ((rc = launch_gemm<32, A_KMAJOR, B_KMAJOR, 128, true, 1, 2, EPK_FWD>(g, ta, tb, s))) return rc;
     } else if (conv1_u8()) {
@@ -940,17 +949,9 @@ struct SampleSpec {
 __global__ void advance_seed_kernel(unsigned long long* seed_state) {
   pdl_trigger();  // the forward's first kernel may launch now (it waits for this one)
   pdl_wait();     // the previous call's sampler has read the seed
-  unsigned long long x = *seed_state + 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  *seed_state = x ^ (x >> 31);
+  advance_seed_dev(seed_state);
 }
 
-static int advance_seed(const SampleSpec* smp, cudaStream_t s) {
-  if (!smp || !smp->seed_state) return BP_OK;
-  launch_pdl(advance_seed_kernel, dim3(1), dim3(1), 0, s, smp->seed_state);
-  return check_launch("advance_seed_kernel");
-}
 
 static int heads_forward(const BpAtariNet* net, int n, const void* head_in, float* logits, float* baseline,
                          cudaStream_t s, const SampleSpec* smp = nullptr) {
@@ -1000,14 +1001,15 @@ static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 0, off);
   int rc;
-  if ((rc = advance_seed(smp, s))) return rc;
+  unsigned long long* seed_state = smp ? smp->seed_state : nullptr;  // advanced by the torso's first kernel
   // small inference batches (no backward follows): split-K fc + CUDA-core heads and sampling
   const int mt = (n + 127) / 128;
   int S = 148 / (mt * 8);
   S = S > 7 ? 7 : S;
   if (smp && (net->flags & BP_NET_NO_X0) && n <= kInferSmallN && S >= 2 && small_infer() &&
       (size_t)S * n * 512 * sizeof(float) <= net->ws_bytes) {
-    if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s, S)))
+    if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s, S,
+                            seed_state)))
       return rc;
     launch_pdl(infer_heads_kernel, dim3(n), dim3(128), 0, s, reinterpret_cast<const float*>(net->ws), S,
                (long long)n * 512, params + off[P_BFC], reinterpret_cast<const __nv_bfloat16*>(net->core),
@@ -1015,7 +1017,8 @@ static int atari_forward(const BpAtariNet* net, int n, const uint8_t* frames, co
                smp->seed, (const unsigned long long*)smp->seed_state, smp->greedy);
     return check_launch("infer_heads_kernel");
   }
-  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
+  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s, 1,
+                          seed_state)))
     return rc;
   return heads_forward(net, n, net->core, logits, baseline, s, smp);
 }
@@ -1577,8 +1580,8 @@ static int atari_lstm_forward(const BpAtariNet* net, const BpLstmCore* core, int
   int64_t off[P_COUNT + 1];
   param_offsets(net->num_actions, 1, off);
   int rc;
-  if ((rc = advance_seed(smp, s))) return rc;
-  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s)))
+  if ((rc = torso_forward(net, n, frames, plane_index, num_planes, reward, last_action, params, off, s, 1,
+                          smp ? smp->seed_state : nullptr)))
     return rc;
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(core->wih);
   const size_t wsz = (size_t)G4 * kCoreW;

@@ -50,7 +50,17 @@ struct PrepArgs {
   const int64_t* last_action;
   __nv_bfloat16* core;
   int n, A;  // n == 0: no prep work
+  unsigned long long* seed_state;  // non-null: advance the sampler's device-resident seed once
 };
+
+// graph-replayable sampling: every forward advances the device-resident seed (splitmix64 step)
+// before its heads read it
+BP_DEVICE void advance_seed_dev(unsigned long long* seed_state) {
+  unsigned long long x = *seed_state + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  *seed_state = x ^ (x >> 31);
+}
 
 BP_DEVICE void prep_items(const PrepArgs& p, long long i0, long long stride) {
   constexpr int W = 576;
@@ -835,6 +845,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, AM, BM, BSWZ, BRES, AW, AU8>::THRE
       if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 3 && g.prep.n > 0) {
+    if (blockIdx.x == 0 && lane == 0 && g.prep.seed_state) advance_seed_dev(g.prep.seed_state);
     prep_items(g.prep, (long long)blockIdx.x * 32 + lane, (long long)gridDim.x * 32);
   } else if (warp >= 4 && warp < 4 + 4 * C::EPI) {
     // epilogue warpgroup grp takes the CTA's tiles k = grp, grp + EPI, ... (accumulator k % ACC);
