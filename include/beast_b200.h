@@ -325,11 +325,11 @@ size_t bp_lstm_partial_floats(int hidden);
  * DSMEM exchange when available, else the grid-cooperative kernels), 1 cooperative,
  * 2 cluster.  Process-wide; for tests and diagnostics. */
 int bp_lstm_set_mode(int mode);
-/* 1 if the LSTM recurrence currently runs on the cluster kernels (bf16 recurrent operands),
- * 0 if on the cooperative f32 kernels. */
 /* Diagnostics: how many 16-CTA recurrence clusters can be co-resident (8 batch columns each;
  * 7 on a 148-SM B200, so B <= 56 runs as one pass). */
 int bp_lstm_cluster_capacity(void);
+/* 1 if the LSTM recurrence currently runs on the cluster kernels (bf16 recurrent operands),
+ * 0 if on the cooperative f32 kernels. */
 int bp_lstm_cluster_active(void);
 /* Diagnostics: per-step %globaltimer trace of CTA 0 of the recurrent kernels into
  * buf (device u64 [2][T1][4] + 2: forward phases, backward phases, forward start /
