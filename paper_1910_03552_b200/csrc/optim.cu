@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(kOptThreads) sumsq_kernel(const float* __restr
                                                             double* __restrict__ out,
                                                             double* __restrict__ partials,
                                                             unsigned* __restrict__ counter) {
+  pdl_trigger();  // the update may launch once every block has started; it waits for this kernel
   pdl_wait();
   const int64_t tid = (int64_t)blockIdx.x * kOptThreads + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kOptThreads;
